@@ -1,0 +1,172 @@
+/*
+ * frr.h -- C-ABI of libfrr.so, the B200 (sm_100a) rerandomization hot path.
+ *
+ * This is the drop-in boundary under the fastrr-compatible Python API
+ * (paper_2501_07642_b200/).  Every entry point replaces one hot function of
+ * the reference fastrr package (arXiv 2501.07642; reference paths below are
+ * relative to pkg/src/fastrr/ of the reference).  The reference has no
+ * native FFI of its own (it is pure numpy), so these are the symbols a
+ * ctypes binding of that path binds; see INTEGRATION.md.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes, no torch types.
+ *   - Every array argument is a DEVICE pointer owned by the caller unless
+ *     its name ends in _host.  Every call is asynchronous on `stream`
+ *     (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Return value: FRR_OK (0) or an error code mirroring fastrr.errors
+ *     (errors.py:9-88); frr_last_error() gives a thread-local message.
+ *   - The library holds no global mutable state besides that message and
+ *     per-device one-time kernel attributes; functions are reentrant.
+ *   - n_units <= FRR_MAX_UNITS (uint16 positions in the generators).
+ */
+#ifndef FRR_H
+#define FRR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRR_ABI_VERSION 1
+#define FRR_MAX_UNITS 65535
+
+enum frr_status {
+    FRR_OK = 0,
+    FRR_E_INVALID_DESIGN = 1,   /* errors.py InvalidDesignError    */
+    FRR_E_DIMENSION = 2,        /* errors.py DimensionError        */
+    FRR_E_ENUM_TOO_LARGE = 3,   /* errors.py EnumerationTooLargeError */
+    FRR_E_STORAGE_CAP = 4,      /* errors.py StorageCapError       */
+    FRR_E_UNSUPPORTED = 5,      /* shape outside the compiled kernels */
+    FRR_E_CUDA = 64             /* CUDA launch / runtime failure    */
+};
+
+/* Integer balance machinery on device (balance.py:75-105).
+ * zq      : int64 [n*d] row-major, the reference's integer-valued Zq
+ * cc      : fp64 [d], fl(colsum_j * fl(1/nc))            (balance.py:97)
+ * colsum  : int64 [d], sum_i zq[i][j] (exact)
+ * g       : fl(fl(1/t) + fl(1/nc))                        (balance.py:96)
+ * cst     : fl(fl((t*nc)/n) * inv_scale_sq)               (balance.py:98)
+ * limbs   : int8 [frr_limbs_bytes()] B operand of the tensor-core path,
+ *           built by frr_prepare_limbs(); NULL when not prepared.      */
+typedef struct frr_balance {
+    int32_t n, d, t, n_limbs;
+    const int64_t* zq;
+    const int64_t* colsum;
+    const double* cc;
+    const int8_t* limbs;
+    double g;
+    double cst;
+} frr_balance_t;
+
+int frr_abi_version(void);
+const char* frr_last_error(void);
+/* number of SMs / compute capability of the current device */
+int frr_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- balance-operand preparation ------------------------------------- */
+/* Bytes of the tiled int8-limb B operand for (n, d, n_limbs). */
+size_t frr_limbs_bytes(int n, int d, int n_limbs);
+/* Split zq into n_limbs balanced int8 digits and tile them in the tcgen05
+ * K-major canonical layout.  *overflow_dev (int32, zeroed by the call) is set
+ * when some |zq| does not fit n_limbs digits.  Replaces the float64 GEMM
+ * operand of balance.py:100-102. */
+int frr_prepare_limbs(const int64_t* zq, int n, int d, int n_limbs, int8_t* limbs,
+                      int32_t* overflow_dev, void* stream);
+
+/* ---- candidate generation + balance check (pass 1) ------------------- */
+/* Monte Carlo draws [draw_lo, draw_lo+count) of root_seed: assignment by
+ * keys.py:138-159 (bit-exact), statistic by balance.py:93-105 (bit-exact).
+ * Replaces generation.py:185-204 (_pass1_stats). */
+int frr_mc_stats(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                 double* stats, void* stream);
+/* Exact enumeration ranks [rank_lo, rank_lo+count) in itertools.combinations
+ * order.  Replaces generation.py:257-272 + 293-296. */
+int frr_exact_stats(const frr_balance_t* bal, uint64_t rank_lo, int64_t count, double* stats,
+                    void* stream);
+/* Exact-mode statistics for an explicit list of lexicographic ranks (any
+ * n, any d; used when frr_exact_stats' n <= 64, d <= 16 kernel does not
+ * apply and for regenerated accepted ranks). */
+int frr_exact_stats_ids(const frr_balance_t* bal, const uint64_t* ranks, int64_t m, double* stats,
+                        void* stream);
+/* Path-forcing variants of frr_mc_stats (frr_mc_stats dispatches): the
+ * CUDA-core warp path and the tcgen05 tensor-core path (FRR_E_UNSUPPORTED
+ * when the shape or limbs do not fit it). */
+int frr_mc_stats_small(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                       double* stats, void* stream);
+int frr_mc_stats_tc(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                    double* stats, void* stream);
+/* Explicit int8 rows [m, n] all treating bal->t units.  Replaces
+ * balance.py:234-251 (batch_balance) per treated-count group. */
+int frr_rows_stats(const frr_balance_t* bal, const int8_t* rows, int64_t m, double* stats,
+                   void* stream);
+
+/* ---- assignment regeneration ------------------------------------------ */
+/* keys (root_seed, draws[i]) -> int8 rows [m, n] and/or packed bits
+ * [m, ceil(n/32)] (bit e of word e/32 = unit e treated).  Either output may
+ * be NULL.  Replaces keys.py:177-208 and generation.py:338-362. */
+int frr_regen_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t,
+                 int8_t* rows, uint32_t* bits, void* stream);
+/* lexicographic ranks -> rows/bits (generation.py:257-272). */
+int frr_regen_exact(const uint64_t* ranks, int64_t m, int n, int t, int8_t* rows, uint32_t* bits,
+                    void* stream);
+
+/* ---- acceptance: exact k-smallest selection (generation.py:159-169) ---- */
+/* Device state of the radix select; the caller allocates it (device) and
+ * initialises it with frr_select_init. */
+typedef struct frr_select_state {
+    uint64_t prefix;   /* threshold bit pattern found so far            */
+    uint64_t mask;     /* bits of prefix that are fixed                 */
+    int64_t k_rem;     /* rank (1-based) still to find inside the prefix */
+    int64_t pad;
+} frr_select_state_t;
+
+int frr_select_init(frr_select_state_t* st, int64_t k, void* stream);
+/* 8-bit digit histogram (pass 0..7, most significant digit first) of the
+ * stats whose bits match st->prefix under st->mask; hist: uint64[256],
+ * zeroed by the call. */
+int frr_select_hist(const double* stats, int64_t m, const frr_select_state_t* st, int pass,
+                    uint64_t* hist, void* stream);
+/* pick the digit holding rank st->k_rem from a (possibly all-reduced) hist */
+int frr_select_pick(const uint64_t* hist, frr_select_state_t* st, int pass, void* stream);
+/* counts[0] = #{stat < T}, counts[1] = #{stat == T}, T = st->prefix */
+int frr_select_count(const double* stats, int64_t m, const frr_select_state_t* st,
+                     int64_t* counts, void* stream);
+/* Order-preserving compaction: accepted = {i: stat<T} plus the first
+ * *tie_quota indices with stat==T; writes ascending (index_base+i) to
+ * idx_out, the stats to stat_out, the count to *n_out.  workspace:
+ * frr_select_workspace_bytes(m) bytes. */
+size_t frr_select_workspace_bytes(int64_t m);
+int frr_select_compact(const double* stats, int64_t m, int64_t index_base,
+                       const frr_select_state_t* st, const int64_t* tie_quota, int64_t* idx_out,
+                       double* stat_out, int64_t* n_out, void* workspace, void* stream);
+
+/* ---- randomization test (inference.py:82-101, 129-182) ----------------- */
+/* Difference in means of y per assignment with numpy's pairwise reduction
+ * order (a), the same for y = obs assignment via popcounts (b), and whether
+ * the row equals the observed assignment (match, atomically OR-ed; may be
+ * NULL).  obs_bits: packed observed assignment; t: treated count of the rows.
+ * Sources: keys (frr_dim_mc), ranks (frr_dim_exact), rows (frr_dim_rows). */
+int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t,
+               const double* y, const uint32_t* obs_bits, double* a, double* b, int32_t* match,
+               void* stream);
+int frr_dim_exact(const uint64_t* ranks, int64_t m, int n, int t, const double* y,
+                  const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream);
+int frr_dim_rows(const int8_t* rows, int64_t m, int n, int t, const double* y,
+                 const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream);
+/* counts[j] = #{i : |a_i - fl(taus[j]*b_i)| >= rhs[j]} for j < ntau
+ * (inference.py:151 with taus=0, inference.py:177-180 p_at). */
+int frr_tau_counts(const double* a, const double* b, int64_t m, const double* taus,
+                   const double* rhs, int ntau, uint64_t* counts, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------ */
+/* D[128 x N] = A[128 x K] . B[N x K]^T (int8 row-major in, int32 out) on one
+ * CTA through the same tcgen05 descriptor code as the fused kernel. */
+int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t* D, int variant,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRR_H */

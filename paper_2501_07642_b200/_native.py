@@ -1,0 +1,143 @@
+"""ctypes binding of libfrr.so (include/frr.h) -- the only path to compute.
+
+The CUDA library is mandatory: there is no CPU fallback.  Importing the
+package works without a GPU (so host-only helpers and validation can be
+used and tested), but every compute entry point raises
+:class:`~paper_2501_07642_b200.errors.NativeUnavailableError` when
+libfrr.so or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("FRR_LIBRARY", os.path.join(_HERE, "libfrr.so"))
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "frr.h")
+
+FRR_OK = 0
+_CODE_TO_ERROR = {
+    1: E.InvalidDesignError,
+    2: E.DimensionError,
+    3: E.EnumerationTooLargeError,
+    4: E.StorageCapError,
+    5: E.UnsupportedShapeError,
+    64: E.DeviceError,
+}
+
+u64, i64, i32, dbl, vp, sz = (ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                              ctypes.c_void_p, ctypes.c_size_t)
+
+
+class Balance(ctypes.Structure):
+    """Mirror of ``frr_balance_t``."""
+
+    _fields_ = [
+        ("n", ctypes.c_int32), ("d", ctypes.c_int32), ("t", ctypes.c_int32), ("n_limbs", ctypes.c_int32),
+        ("zq", vp), ("colsum", vp), ("cc", vp), ("limbs", vp),
+        ("g", dbl), ("cst", dbl),
+    ]
+
+
+SIGNATURES = {
+    "frr_abi_version": (i32, []),
+    "frr_last_error": (ctypes.c_char_p, []),
+    "frr_device_info": (i32, [ctypes.POINTER(i32)] * 3),
+    "frr_limbs_bytes": (sz, [i32, i32, i32]),
+    "frr_prepare_limbs": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "frr_mc_stats": (i32, [ctypes.POINTER(Balance), u64, u64, i64, vp, vp]),
+    "frr_mc_stats_small": (i32, [ctypes.POINTER(Balance), u64, u64, i64, vp, vp]),
+    "frr_mc_stats_tc": (i32, [ctypes.POINTER(Balance), u64, u64, i64, vp, vp]),
+    "frr_exact_stats": (i32, [ctypes.POINTER(Balance), u64, i64, vp, vp]),
+    "frr_exact_stats_ids": (i32, [ctypes.POINTER(Balance), vp, i64, vp, vp]),
+    "frr_rows_stats": (i32, [ctypes.POINTER(Balance), vp, i64, vp, vp]),
+    "frr_regen_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp]),
+    "frr_regen_exact": (i32, [vp, i64, i32, i32, vp, vp, vp]),
+    "frr_select_init": (i32, [vp, i64, vp]),
+    "frr_select_hist": (i32, [vp, i64, vp, i32, vp, vp]),
+    "frr_select_pick": (i32, [vp, vp, i32, vp]),
+    "frr_select_count": (i32, [vp, i64, vp, vp, vp]),
+    "frr_select_workspace_bytes": (sz, [i64]),
+    "frr_select_compact": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "frr_dim_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "frr_dim_exact": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "frr_dim_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "frr_tau_counts": (i32, [vp, vp, i64, vp, vp, i32, vp, vp]),
+    "frr_selftest_mma_i8": (i32, [vp, vp, i32, i32, vp, i32, vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load libfrr.so and bind every exported symbol (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise E.NativeUnavailableError(
+                f"libfrr.so not found at {p}; build it with `python __graft_entry__.py` "
+                "(make -C paper_2501_07642_b200/csrc)")
+        lib = ctypes.CDLL(p)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.frr_abi_version() != 1:
+            raise E.NativeUnavailableError("libfrr.so ABI version mismatch")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def lib() -> ctypes.CDLL:
+    return _lib if _lib is not None else load_library()
+
+
+_torch = None
+
+
+def torch_mod():
+    global _torch
+    if _torch is None:
+        import torch
+
+        _torch = torch
+    return _torch
+
+
+def device():
+    """The CUDA device compute runs on (current device); fails loudly."""
+    torch = torch_mod()
+    if not torch.cuda.is_available():
+        raise E.NativeUnavailableError(
+            "no CUDA device: the rerandomization engine runs only on the GPU (no CPU fallback)")
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr():
+    torch = torch_mod()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def check(rc: int, what: str):
+    if rc != FRR_OK:
+        msg = lib().frr_last_error().decode(errors="replace")
+        cls = _CODE_TO_ERROR.get(rc, E.DeviceError)
+        raise cls(f"{what}: {msg}")
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)

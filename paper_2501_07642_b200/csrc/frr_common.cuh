@@ -1,0 +1,221 @@
+// frr_common.cuh -- shared device code for libfrr (sm_100a).
+//
+// Bit-exact restatement, on the GPU, of the reference key -> assignment
+// contract (keys.py:9-38, 138-159) and of numpy's pairwise reduction order
+// used by balance.py:104 and inference.py:97-98.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/frr.h"
+
+#define FRR_GOLDEN 0x9E3779B97F4A7C15ull
+#define FRR_FULL 0xffffffffu
+#define FRR_CTL 0xFFFFu  // table marker: unit is a control unit
+
+// ---------------------------------------------------------------- error state
+void frr_set_error(const char* fmt, ...);
+int frr_check_launch(const char* what);
+
+// -------------------------------------------------------------- splitmix64
+// keys.py:99-104
+__device__ __forceinline__ uint64_t frr_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// keys.py:118-121
+__device__ __forceinline__ uint64_t frr_derive_state(uint64_t seed, uint64_t draw) {
+    return frr_mix64((seed ^ (draw * FRR_GOLDEN)) + FRR_GOLDEN);
+}
+
+// Per Fisher-Yates step k (bound b = n - k) constants for an exact
+// u mod b without a division:  y = hi(u)*c2 + lo(u)  (c2 = 2^32 mod b,
+// y < 2^48, y == u mod b), then Lemire-Kaser-Kurz direct remainder with
+// M = ceil(2^64 / b), valid for 48-bit dividends and b <= 2^16.
+struct __align__(16) StepC {
+    uint32_t b;
+    uint32_t c2;
+    uint64_t M;
+};
+
+__device__ __forceinline__ StepC frr_make_step(int n, int k) {
+    StepC s;
+    s.b = (uint32_t)(n - k);
+    s.c2 = (uint32_t)((1ull << 32) % s.b);
+    s.M = (~0ull) / s.b + 1ull;
+    return s;
+}
+
+__device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s) {
+    uint64_t y = (uint64_t)(uint32_t)(u >> 32) * s.c2 + (uint32_t)u;
+    uint64_t low = s.M * y;
+    uint64_t hi = (uint64_t)(uint32_t)(low >> 32) * s.b + __umulhi((uint32_t)low, s.b);
+    return (uint32_t)(hi >> 32);
+}
+
+__device__ inline void frr_fill_steps(StepC* steps, int n, int t) {
+    for (int k = threadIdx.x; k < t; k += blockDim.x) steps[k] = frr_make_step(n, k);
+}
+
+// Table words needed per candidate: n uint16 entries padded to 8 (16 bytes).
+__host__ __device__ __forceinline__ int frr_table_len(int n) { return (n + 7) & ~7; }
+
+__device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, int lane) {
+    uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
+    uint4 q = make_uint4(w, w, w, w);
+    int len = frr_table_len(n);
+    for (int i = lane * 8; i < len; i += 256) *reinterpret_cast<uint4*>(lw + i) = q;
+}
+
+// ----------------------------------------------------------- warp generator
+// One warp builds the assignment of draw (seed, draw) into the per-warp table
+// lw[0..n): on return lw[e] == FRR_CTL iff unit e is a control unit.
+//
+// Equivalent to the reference's sequential partial Fisher-Yates
+// (keys.py:146-158) but parallel over the t steps: the stream value of step
+// k is mix64(state + (k+1)C) unless an earlier step rejected, which needs
+// hi(u) == 0xFFFFFFFF (p ~ 2^-32); any such warp redoes the candidate
+// sequentially with exact rejection.  Swaps are replaced by a "last writer"
+// table: lw[p] = 1 + (last step k < p with r_k = p).  The final content of a
+// position p >= t is found by following lw links to a never-written position
+// (its original element); those t..n-1 contents are the control units.
+__device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
+                                            uint16_t* lw, int lane) {
+    frr_table_fill(lw, n, 0, lane);
+    __syncwarp();
+    bool flag = false;
+    uint64_t x = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
+    const uint64_t stride = 32ull * FRR_GOLDEN;
+    for (int base = 0; base < t; base += 32) {
+        int k = base + lane;
+        bool pend = false;
+        uint32_t r = 0;
+        if (k < t) {
+            uint64_t u = frr_mix64(x);
+            StepC s = steps[k];
+            flag |= ((uint32_t)(u >> 32) == 0xFFFFFFFFu);
+            uint32_t rem = frr_mod_step(u, s);
+            r = (uint32_t)k + rem;
+            pend = rem != 0;
+        }
+        x += stride;
+        // last writer wins: later rounds overwrite, ties inside a round are
+        // settled by re-reading until the largest k of the round holds r
+        while (__any_sync(FRR_FULL, pend)) {
+            if (pend) lw[r] = (uint16_t)(k + 1);
+            __syncwarp();
+            if (pend) pend = lw[r] < (uint16_t)(k + 1);
+            __syncwarp();
+        }
+    }
+    if (__any_sync(FRR_FULL, flag)) {
+        // exact sequential restatement with rejection (keys.py:146-156)
+        __syncwarp();
+        frr_table_fill(lw, n, 0, lane);
+        __syncwarp();
+        if (lane == 0) {
+            uint64_t s = state;
+            for (int j = 0; j < t; j++) {
+                uint64_t b = (uint64_t)(n - j);
+                uint64_t rem = (0ull - b) % b;
+                uint64_t u;
+                do {
+                    s += FRR_GOLDEN;
+                    u = frr_mix64(s);
+                } while (rem != 0 && u >= 0ull - rem);
+                uint32_t r = (uint32_t)j + (uint32_t)(u % b);
+                if (r != (uint32_t)j) lw[r] = (uint16_t)(j + 1);
+            }
+        }
+        __syncwarp();
+    }
+    for (int p = t + lane; p < n; p += 32) {
+        int q = p;
+        uint32_t v = lw[q];
+        while (v != 0) {
+            q = (int)v - 1;
+            v = lw[q];
+        }
+        lw[q] = FRR_CTL;  // each chain ends at its own root: no other lane reads it
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------- exact (combinadic)
+// generation.py:257-266: itertools.combinations order == lexicographic
+// combinadic unranking.  binom(a, b) exact in 64 bits for a <= 67.
+__device__ __forceinline__ uint64_t frr_binom(int a, int b) {
+    if (b < 0 || b > a) return 0;
+    if (b > a - b) b = a - b;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= b; i++) r = r * (unsigned)(a - b + i) / (unsigned)i;
+    return (uint64_t)r;
+}
+
+// Writes the t treated units of lexicographic rank `rank` into table lw as
+// "not control" (others FRR_CTL).  Single lane, any n.
+__device__ inline void frr_unrank_to_table(uint64_t rank, int n, int t, uint16_t* lw) {
+    int x = 0;
+    for (int i = 0; i < t; i++) {
+        // C(n-x-1, t-i-1) as x advances, updated multiplicatively
+        int a = n - x - 1, b = t - i - 1;
+        unsigned __int128 c = frr_binom(a, b);
+        while (rank >= (uint64_t)c) {
+            rank -= (uint64_t)c;
+            // C(a-1, b) = C(a, b) * (a - b) / a
+            c = c * (unsigned)(a - b) / (unsigned)a;
+            a--;
+            x++;
+        }
+        lw[x] = 0;
+        x++;
+    }
+}
+
+// --------------------------------------------------------- pairwise sums
+// numpy pairwise_sum (PW_BLOCKSIZE 128) on a leaf of length len, values
+// produced by f(i) for i in [0, len).
+template <class F>
+__device__ __forceinline__ double frr_pw_leaf(int len, F f) {
+    if (len < 8) {
+        double res = -0.0;
+        for (int i = 0; i < len; i++) res = __dadd_rn(res, f(i));
+        return res;
+    }
+    double r0 = f(0), r1 = f(1), r2 = f(2), r3 = f(3), r4 = f(4), r5 = f(5), r6 = f(6), r7 = f(7);
+    int i = 8;
+    int full = len - (len % 8);
+    for (; i < full; i += 8) {
+        r0 = __dadd_rn(r0, f(i + 0));
+        r1 = __dadd_rn(r1, f(i + 1));
+        r2 = __dadd_rn(r2, f(i + 2));
+        r3 = __dadd_rn(r3, f(i + 3));
+        r4 = __dadd_rn(r4, f(i + 4));
+        r5 = __dadd_rn(r5, f(i + 5));
+        r6 = __dadd_rn(r6, f(i + 6));
+        r7 = __dadd_rn(r7, f(i + 7));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                           __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+    for (; i < len; i++) res = __dadd_rn(res, f(i));
+    return res;
+}
+
+// Whole pairwise sum of a[0..n) held in (shared or global) memory; single
+// thread; recursion depth <= log2(n/64).  Returns 0.0 + pw (the reduction
+// starts from the additive identity).
+__device__ inline double frr_pw_rec(const double* a, int n) {
+    if (n <= 128) return frr_pw_leaf(n, [&](int i) { return a[i]; });
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(frr_pw_rec(a, n2), frr_pw_rec(a + n2, n - n2));
+}
+
+__device__ inline double frr_pw_sum(const double* a, int n) { return __dadd_rn(0.0, frr_pw_rec(a, n)); }
+
+// --------------------------------------------------------- small helpers
+__device__ __forceinline__ uint64_t frr_f64_bits(double x) { return (uint64_t)__double_as_longlong(x); }
+
+__host__ __device__ __forceinline__ int64_t frr_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -1,0 +1,640 @@
+// frr_gen.cu -- candidate generation, CUDA-core balance checks, regeneration
+// and the randomization-test kernels (sm_100a).
+//
+// Work mapping: one warp per candidate.  A candidate's assignment lives only
+// in a per-warp shared-memory table (2 bytes per unit) and is consumed in
+// place; nothing per candidate but its statistic reaches HBM.
+#include <cuda_runtime.h>
+
+#include "frr_common.cuh"
+#include "frr_launch.cuh"
+
+namespace {
+
+constexpr int kWarps = 8;  // warps per CTA for the warp-per-candidate kernels
+constexpr int kThreads = kWarps * 32;
+
+enum Source { SRC_KEYS = 0, SRC_RANKS = 1, SRC_ROWS = 2 };
+
+// Build the candidate table for source SRC.
+template <int SRC>
+__device__ __forceinline__ void build_table(uint64_t seed, const uint64_t* ids, const int8_t* rows,
+                                            int64_t c, int n, int t, const StepC* steps, uint16_t* lw,
+                                            int lane) {
+    if (SRC == SRC_KEYS) {
+        frr_warp_fy(frr_derive_state(seed, ids[c]), n, t, steps, lw, lane);
+    } else if (SRC == SRC_RANKS) {
+        frr_table_fill(lw, n, FRR_CTL, lane);
+        __syncwarp();
+        if (lane == 0) frr_unrank_to_table(ids[c], n, t, lw);
+        __syncwarp();
+    } else {
+        const int8_t* row = rows + (size_t)c * n;
+        for (int e = lane; e < n; e += 32) lw[e] = row[e] ? (uint16_t)0 : (uint16_t)FRR_CTL;
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ uint32_t table_word(const uint16_t* lw, int n, int w) {
+    uint32_t word = 0;
+    int e0 = w * 32;
+#pragma unroll 8
+    for (int i = 0; i < 32; i++) {
+        int e = e0 + i;
+        if (e < n && lw[e] != FRR_CTL) word |= 1u << i;
+    }
+    return word;
+}
+
+// ------------------------------------------------------------- regeneration
+template <int SRC>
+__global__ void __launch_bounds__(kThreads) k_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n,
+                                                    int t, int8_t* rows, uint32_t* bits) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    StepC* steps = reinterpret_cast<StepC*>(smem);
+    int nsteps = SRC == SRC_KEYS ? t : 0;
+    uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
+    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
+    __syncthreads();
+    const int words = (n + 31) >> 5;
+    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < m; c += (int64_t)gridDim.x * kWarps) {
+        build_table<SRC>(seed, ids, nullptr, c, n, t, steps, lw, lane);
+        if (rows) {
+            int8_t* out = rows + (size_t)c * n;
+            if ((n & 7) == 0) {
+                for (int e = lane * 8; e < n; e += 256) {
+                    uint32_t lo = 0, hi = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; i++) lo |= (uint32_t)(lw[e + i] != FRR_CTL) << (8 * i);
+#pragma unroll
+                    for (int i = 0; i < 4; i++) hi |= (uint32_t)(lw[e + 4 + i] != FRR_CTL) << (8 * i);
+                    *reinterpret_cast<uint2*>(out + e) = make_uint2(lo, hi);
+                }
+            } else {
+                for (int e = lane; e < n; e += 32) out[e] = lw[e] != FRR_CTL;
+            }
+        }
+        if (bits) {
+            uint32_t* ob = bits + (size_t)c * words;
+            for (int w = lane; w < words; w += 32) ob[w] = table_word(lw, n, w);
+        }
+        __syncwarp();
+    }
+}
+
+// -------------------------------------------------------- small-d epilogue
+// balance.py:96-104 for d <= D: delta = fl(fl(S*g) - cc); q = delta^2;
+// numpy pairwise sum over the d values; times const.
+template <int D>
+__device__ __forceinline__ double small_stat(const int64_t (&S)[D], int d, double g, const double* cc,
+                                             double cst) {
+    double q[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        if (j < d) {
+            double delta = __dsub_rn(__dmul_rn(__ll2double_rn(S[j]), g), cc[j]);
+            q[j] = __dmul_rn(delta, delta);
+        } else {
+            q[j] = 0.0;
+        }
+    }
+    double res;
+    if (d < 8) {
+        res = -0.0;
+#pragma unroll
+        for (int j = 0; j < D; j++)
+            if (j < d) res = __dadd_rn(res, q[j]);
+    } else {
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) r[k] = q[k < D ? k : 0];
+        int full = d - (d % 8);
+        if (D >= 16 && full >= 16) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], q[(8 + k) < D ? 8 + k : 0]);
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+        for (int j = 8; j < D; j++)
+            if (j >= full && j < d) res = __dadd_rn(res, q[j]);
+    }
+    return __dmul_rn(__dadd_rn(0.0, res), cst);
+}
+
+template <int D>
+__device__ __forceinline__ void warp_sum(int64_t (&a)[D]) {
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a[j] += __shfl_xor_sync(FRR_FULL, a[j], o);
+    }
+}
+
+// ------------------------------------------------ small-d balance (d <= 16)
+// S = colsum - sum over control units of Zq rows (exact int64), warp
+// reduction, then the fp64 epilogue on lane 0.
+template <int SRC, int D>
+__global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
+                                                          const int8_t* rows, uint64_t lo, int64_t count,
+                                                          double* out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = bal.n, t = bal.t, d = bal.d;
+    StepC* steps = reinterpret_cast<StepC*>(smem);
+    int nsteps = SRC == SRC_KEYS ? t : 0;
+    uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
+    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
+    __syncthreads();
+    const int64_t* __restrict__ zq = bal.zq;
+    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < count; c += (int64_t)gridDim.x * kWarps) {
+        if (SRC == SRC_KEYS) {
+            frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
+        } else {
+            build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+        }
+        int64_t acc[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) acc[j] = 0;
+        for (int e = lane; e < n; e += 32) {
+            if (lw[e] == FRR_CTL) {
+                const int64_t* z = zq + (size_t)e * d;
+#pragma unroll
+                for (int j = 0; j < D; j++)
+                    if (j < d) acc[j] += __ldg(reinterpret_cast<const long long*>(z) + j);
+            }
+        }
+        warp_sum<D>(acc);
+        if (lane == 0) {
+            int64_t S[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) S[j] = j < d ? bal.colsum[j] - acc[j] : 0;
+            out[c] = small_stat<D>(S, d, bal.g, bal.cc, bal.cst);
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------- generic balance (any d)
+// Lanes own columns j; S_j = colsum_j - sum_{control e} Zq[e][j]; q_j to a
+// per-warp scratch; lane 0 runs the exact numpy pairwise sum.
+template <int SRC>
+__global__ void __launch_bounds__(kThreads) k_stats_generic(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
+                                                            const int8_t* rows, uint64_t lo, int64_t count,
+                                                            double* out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = bal.n, t = bal.t, d = bal.d;
+    StepC* steps = reinterpret_cast<StepC*>(smem);
+    int nsteps = SRC == SRC_KEYS ? t : 0;
+    double* scratch = reinterpret_cast<double*>(steps + nsteps);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (size_t)kWarps * d);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
+    double* q = scratch + (size_t)warp * d;
+    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
+    __syncthreads();
+    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < count; c += (int64_t)gridDim.x * kWarps) {
+        if (SRC == SRC_KEYS) {
+            frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
+        } else {
+            build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+        }
+        for (int j = lane; j < d; j += 32) {
+            int64_t acc = 0;
+            for (int e = 0; e < n; e++)
+                if (lw[e] == FRR_CTL) acc += bal.zq[(size_t)e * d + j];
+            int64_t S = bal.colsum[j] - acc;
+            double delta = __dsub_rn(__dmul_rn(__ll2double_rn(S), bal.g), bal.cc[j]);
+            q[j] = __dmul_rn(delta, delta);
+        }
+        __syncwarp();
+        if (lane == 0) out[c] = __dmul_rn(frr_pw_sum(q, d), bal.cst);
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------- exact enumeration (n <= 64)
+// One lane walks a run of 32 consecutive lexicographic ranks: unrank once,
+// then the complement-Gosper successor (unit i <-> bit n-1-i, lex order ==
+// decreasing mask) with an incremental exact S.  Results are transposed
+// through shared memory for coalesced stores.
+constexpr int kRun = 32;
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uint64_t rank_lo, int64_t count,
+                                                          double* out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = bal.n, t = bal.t, d = bal.d;
+    uint64_t* binom = reinterpret_cast<uint64_t*>(smem);              // [65][65]
+    int64_t* zq = reinterpret_cast<int64_t*>(binom + 65 * 65);       // [n][D]
+    double* stage = reinterpret_cast<double*>(zq + (size_t)n * D);   // [kWarps][32][33]
+    for (int i = threadIdx.x; i < 65 * 65; i += blockDim.x) binom[i] = frr_binom(i / 65, i % 65);
+    for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
+        int e = i / D, j = i % D;
+        zq[i] = j < d ? bal.zq[(size_t)e * d + j] : 0;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* st = stage + (size_t)warp * 32 * 33;
+    const uint64_t fullmask = n == 64 ? ~0ull : ((1ull << n) - 1ull);
+    const int64_t per_warp = 32 * kRun;
+    for (int64_t wb = ((int64_t)blockIdx.x * kWarps + warp) * per_warp; wb < count;
+         wb += (int64_t)gridDim.x * kWarps * per_warp) {
+        int64_t r0 = wb + (int64_t)lane * kRun;
+        int64_t left = count - r0;
+        int nrun = left < kRun ? (int)left : kRun;
+        if (nrun > 0) {
+            // unrank rank_lo + r0 into mask (unit i <-> bit n-1-i)
+            uint64_t rank = rank_lo + (uint64_t)r0;
+            uint64_t m = 0;
+            int x = 0;
+            for (int i = 0; i < t; i++) {
+                for (;;) {
+                    uint64_t cnk = binom[(n - x - 1) * 65 + (t - i - 1)];
+                    if (rank < cnk) break;
+                    rank -= cnk;
+                    x++;
+                }
+                m |= 1ull << (n - 1 - x);
+                x++;
+            }
+            int64_t S[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) S[j] = 0;
+            uint64_t mm = m;
+            while (mm) {
+                int b = __ffsll((long long)mm) - 1;
+                const int64_t* z = zq + (size_t)(n - 1 - b) * D;
+#pragma unroll
+                for (int j = 0; j < D; j++) S[j] += z[j];
+                mm &= mm - 1;
+            }
+            for (int r = 0; r < nrun; r++) {
+                st[lane * 33 + r] = small_stat<D>(S, d, bal.g, bal.cc, bal.cst);
+                if (r + 1 < nrun) {
+                    uint64_t xc = ~m & fullmask;
+                    uint64_t cbit = xc & (0ull - xc);
+                    uint64_t rr = xc + cbit;
+                    uint64_t xn = (((rr ^ xc) >> 2) >> (__ffsll((long long)cbit) - 1)) | rr;
+                    uint64_t mn = ~xn & fullmask;
+                    uint64_t diff = m ^ mn;
+                    while (diff) {
+                        int b = __ffsll((long long)diff) - 1;
+                        const int64_t* z = zq + (size_t)(n - 1 - b) * D;
+                        if ((mn >> b) & 1ull) {
+#pragma unroll
+                            for (int j = 0; j < D; j++) S[j] += z[j];
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < D; j++) S[j] -= z[j];
+                        }
+                        diff &= diff - 1;
+                    }
+                    m = mn;
+                }
+            }
+        }
+        __syncwarp();
+        for (int k = 0; k < 32; k++) {
+            int64_t idx = wb + (int64_t)k * 32 + lane;
+            if (idx < count) out[idx] = st[(k * 32 + lane) / kRun * 33 + (k * 32 + lane) % kRun];
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------ randomization-test rows
+// inference.py:82-101 (_dim_rows) for y (a) and for the observed assignment
+// as outcome (b, exact popcounts), plus the pool-membership flag
+// (inference.py:144).  The pairwise plan of length n (numpy's recursion) is
+// built once per CTA: leaves + a post-order combine program.
+struct PwPlan {
+    int nleaf, ntok;
+    int* leaf_off;
+    int* leaf_len;
+    int16_t* tok;  // >=0: leaf id; -1: combine
+};
+
+__device__ void plan_build(PwPlan& P, int off, int len) {
+    if (len <= 128) {
+        P.leaf_off[P.nleaf] = off;
+        P.leaf_len[P.nleaf] = len;
+        P.tok[P.ntok++] = (int16_t)P.nleaf++;
+        return;
+    }
+    int n2 = len / 2;
+    n2 -= n2 % 8;
+    plan_build(P, off, n2);
+    plan_build(P, off + n2, len - n2);
+    P.tok[P.ntok++] = -1;
+}
+
+__host__ __device__ inline int plan_max_leaves(int n) { return n / 64 + 2; }
+
+template <int SRC>
+__global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows,
+                                                  int64_t m, int n, int t, const double* __restrict__ y,
+                                                  const uint32_t* __restrict__ obs, double* a, double* b,
+                                                  int32_t* match) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int maxl = plan_max_leaves(n);
+    StepC* steps = reinterpret_cast<StepC*>(smem);
+    int nsteps = SRC == SRC_KEYS ? t : 0;
+    double* leafres = reinterpret_cast<double*>(steps + nsteps);          // [kWarps][2][maxl]
+    int* leaf_off = reinterpret_cast<int*>(leafres + (size_t)kWarps * 2 * maxl);
+    int* leaf_len = leaf_off + maxl;
+    int16_t* tok = reinterpret_cast<int16_t*>(leaf_len + maxl);          // [2*maxl]
+    __shared__ int s_nleaf, s_ntok;
+    uint16_t* tables = reinterpret_cast<uint16_t*>(tok + ((2 * maxl + 7) & ~7));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
+    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
+    if (threadIdx.x == 0) {
+        PwPlan P{0, 0, leaf_off, leaf_len, tok};
+        plan_build(P, 0, n);
+        s_nleaf = P.nleaf;
+        s_ntok = P.ntok;
+    }
+    __syncthreads();
+    const int nleaf = s_nleaf, ntok = s_ntok;
+    double* rt = leafres + (size_t)warp * 2 * maxl;
+    double* rc = rt + maxl;
+    const int words = (n + 31) >> 5;
+    const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
+    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < m; c += (int64_t)gridDim.x * kWarps) {
+        build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+        // b and membership from packed words
+        uint32_t pt = 0, pc = 0;
+        bool same = true;
+        for (int w = lane; w < words; w += 32) {
+            uint32_t word = table_word(lw, n, w);
+            uint32_t o = obs[w];
+            pt += __popc(word & o);
+            pc += __popc(~word & o);
+            same &= (word == o);
+        }
+        // a: masked pairwise sums, one leaf per lane at a time
+        for (int L = lane; L < nleaf; L += 32) {
+            const int off = leaf_off[L], len = leaf_len[L];
+            double st = frr_pw_leaf(len, [&](int i) {
+                int e = off + i;
+                double v = __ldg(y + e);
+                return lw[e] != FRR_CTL ? v : copysign(0.0, v);
+            });
+            double sc = frr_pw_leaf(len, [&](int i) {
+                int e = off + i;
+                double v = __ldg(y + e);
+                return lw[e] != FRR_CTL ? copysign(0.0, v) : v;
+            });
+            rt[L] = st;
+            rc[L] = sc;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            pt += __shfl_xor_sync(FRR_FULL, pt, o);
+            pc += __shfl_xor_sync(FRR_FULL, pc, o);
+        }
+        same = __all_sync(FRR_FULL, same);
+        __syncwarp();
+        if (lane == 0) {
+            double stk_t[24], stk_c[24];
+            int sp = 0;
+            for (int i = 0; i < ntok; i++) {
+                int tk = tok[i];
+                if (tk >= 0) {
+                    stk_t[sp] = rt[tk];
+                    stk_c[sp] = rc[tk];
+                    sp++;
+                } else {
+                    sp--;
+                    stk_t[sp - 1] = __dadd_rn(stk_t[sp - 1], stk_t[sp]);
+                    stk_c[sp - 1] = __dadd_rn(stk_c[sp - 1], stk_c[sp]);
+                }
+            }
+            double s_t = __dadd_rn(0.0, stk_t[0]), s_c = __dadd_rn(0.0, stk_c[0]);
+            a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
+            if (b) b[c] = __dsub_rn(__dmul_rn((double)pt, inv_t), __dmul_rn((double)pc, inv_c));
+            if (match && same) atomicOr(match, 1);
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------ tau counts
+constexpr int kTauTile = 32;
+
+__global__ void __launch_bounds__(256) k_tau_counts(const double* __restrict__ a, const double* __restrict__ b,
+                                                    int64_t m, const double* __restrict__ taus,
+                                                    const double* __restrict__ rhs, int ntau,
+                                                    unsigned long long* counts) {
+    __shared__ double s_tau[kTauTile], s_rhs[kTauTile];
+    const int t0 = blockIdx.y * kTauTile;
+    const int nt = min(kTauTile, ntau - t0);
+    if (threadIdx.x < nt) {
+        s_tau[threadIdx.x] = taus[t0 + threadIdx.x];
+        s_rhs[threadIdx.x] = rhs[t0 + threadIdx.x];
+    }
+    __syncthreads();
+    uint32_t cnt[kTauTile];
+#pragma unroll
+    for (int j = 0; j < kTauTile; j++) cnt[j] = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        double ai = a[i], bi = b[i];
+#pragma unroll
+        for (int j = 0; j < kTauTile; j++) {
+            if (j < nt) cnt[j] += fabs(__dsub_rn(ai, __dmul_rn(s_tau[j], bi))) >= s_rhs[j];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kTauTile; j++) {
+        uint32_t v = cnt[j];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FRR_FULL, v, o);
+        if ((threadIdx.x & 31) == 0 && j < nt && v) atomicAdd(counts + t0 + j, (unsigned long long)v);
+    }
+}
+
+// -------------------------------------------------------- host helpers
+size_t table_bytes(int n) { return (size_t)kWarps * frr_table_len(n) * sizeof(uint16_t); }
+
+int check_nt(int n, int t) {
+    if (n < 2 || n > FRR_MAX_UNITS) {
+        frr_set_error("n_units=%d outside [2, %d]", n, FRR_MAX_UNITS);
+        return n < 2 ? FRR_E_INVALID_DESIGN : FRR_E_UNSUPPORTED;
+    }
+    if (t <= 0 || t >= n) {
+        frr_set_error("n_treated must satisfy 0 < n_treated < n_units (got %d, %d)", t, n);
+        return FRR_E_INVALID_DESIGN;
+    }
+    return FRR_OK;
+}
+
+template <int SRC>
+int launch_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n, int t, int8_t* rows, uint32_t* bits,
+                 void* stream) {
+    int rc = check_nt(n, t);
+    if (rc) return rc;
+    if (m <= 0) return FRR_OK;
+    size_t smem = (SRC == SRC_KEYS ? (size_t)t * sizeof(StepC) : 0) + table_bytes(n);
+    auto kern = k_regen<SRC>;
+    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
+    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(m, kWarps));
+    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(seed, ids, m, n, t, rows, bits);
+    return frr_check_launch("k_regen");
+}
+
+template <int SRC, int D>
+int launch_small(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, const int8_t* rows, uint64_t lo,
+                 int64_t count, double* out, void* stream) {
+    size_t smem = (SRC == SRC_KEYS ? (size_t)bal->t * sizeof(StepC) : 0) + table_bytes(bal->n);
+    auto kern = k_stats_small<SRC, D>;
+    int rc = frr_prepare_kernel(kern, smem);
+    if (rc) return rc;
+    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, kWarps));
+    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, seed, ids, rows, lo, count, out);
+    return frr_check_launch("k_stats_small");
+}
+
+template <int SRC>
+int launch_stats(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, const int8_t* rows, uint64_t lo,
+                 int64_t count, double* out, void* stream) {
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (count <= 0) return FRR_OK;
+    if (bal->d <= 4) return launch_small<SRC, 4>(bal, seed, ids, rows, lo, count, out, stream);
+    if (bal->d <= 8) return launch_small<SRC, 8>(bal, seed, ids, rows, lo, count, out, stream);
+    if (bal->d <= 16) return launch_small<SRC, 16>(bal, seed, ids, rows, lo, count, out, stream);
+    size_t smem = (SRC == SRC_KEYS ? (size_t)bal->t * sizeof(StepC) : 0) + (size_t)kWarps * bal->d * sizeof(double) +
+                  table_bytes(bal->n);
+    if (smem > 227 * 1024) {
+        frr_set_error("generic balance kernel needs %zu B shared memory (d=%d, n=%d)", smem, bal->d, bal->n);
+        return FRR_E_UNSUPPORTED;
+    }
+    auto kern = k_stats_generic<SRC>;
+    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
+    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, kWarps));
+    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, seed, ids, rows, lo, count, out);
+    return frr_check_launch("k_stats_generic");
+}
+
+template <int D>
+int launch_exact_small(const frr_balance_t* bal, uint64_t rank_lo, int64_t count, double* out, void* stream) {
+    size_t smem = 65 * 65 * sizeof(uint64_t) + (size_t)bal->n * D * sizeof(int64_t) +
+                  (size_t)kWarps * 32 * 33 * sizeof(double);
+    auto kern = k_exact_small<D>;
+    int rc = frr_prepare_kernel(kern, smem);
+    if (rc) return rc;
+    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, (int64_t)kWarps * 32 * kRun));
+    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, rank_lo, count, out);
+    return frr_check_launch("k_exact_small");
+}
+
+template <int SRC>
+int launch_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows, int64_t m, int n, int t, const double* y,
+               const uint32_t* obs, double* a, double* b, int32_t* match, void* stream) {
+    int rc = check_nt(n, t);
+    if (rc) return rc;
+    if (m <= 0) return FRR_OK;
+    int maxl = plan_max_leaves(n);
+    size_t smem = (SRC == SRC_KEYS ? (size_t)t * sizeof(StepC) : 0) + (size_t)kWarps * 2 * maxl * sizeof(double) +
+                  2 * (size_t)maxl * sizeof(int) + (size_t)((2 * maxl + 7) & ~7) * sizeof(int16_t) +
+                  table_bytes(n);
+    if (smem > 227 * 1024) {
+        frr_set_error("dim kernel needs %zu B shared memory (n=%d)", smem, n);
+        return FRR_E_UNSUPPORTED;
+    }
+    auto kern = k_dim<SRC>;
+    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
+    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(m, kWarps));
+    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(seed, ids, rows, m, n, t, y, obs, a, b, match);
+    return frr_check_launch("k_dim");
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats,
+                     void* stream);  // frr_mma.cu
+bool frr_mma_supported(const frr_balance_t* bal);
+
+extern "C" int frr_mc_stats(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                            double* stats, void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    if (bal->limbs && frr_mma_supported(bal)) return frr_mc_stats_mma(bal, root_seed, draw_lo, count, stats, stream);
+    return launch_stats<SRC_KEYS>(bal, root_seed, nullptr, nullptr, draw_lo, count, stats, stream);
+}
+
+extern "C" int frr_exact_stats(const frr_balance_t* bal, uint64_t rank_lo, int64_t count, double* stats,
+                               void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (count <= 0) return FRR_OK;
+    if (bal->n <= 64 && bal->d <= 16) {
+        if (bal->d <= 4) return launch_exact_small<4>(bal, rank_lo, count, stats, stream);
+        if (bal->d <= 8) return launch_exact_small<8>(bal, rank_lo, count, stats, stream);
+        return launch_exact_small<16>(bal, rank_lo, count, stats, stream);
+    }
+    // general exact path: ranks materialised on the fly, one per warp
+    frr_set_error("frr_exact_stats: n=%d d=%d needs the rank-list path (use frr_exact_stats_ids)", bal->n, bal->d);
+    return FRR_E_UNSUPPORTED;
+}
+
+extern "C" int frr_exact_stats_ids(const frr_balance_t* bal, const uint64_t* ranks, int64_t m, double* stats,
+                                   void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    return launch_stats<SRC_RANKS>(bal, 0, ranks, nullptr, 0, m, stats, stream);
+}
+
+extern "C" int frr_rows_stats(const frr_balance_t* bal, const int8_t* rows, int64_t m, double* stats,
+                              void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    return launch_stats<SRC_ROWS>(bal, 0, nullptr, rows, 0, m, stats, stream);
+}
+
+extern "C" int frr_mc_stats_small(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                                  double* stats, void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    return launch_stats<SRC_KEYS>(bal, root_seed, nullptr, nullptr, draw_lo, count, stats, stream);
+}
+
+extern "C" int frr_regen_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t, int8_t* rows,
+                            uint32_t* bits, void* stream) {
+    return launch_regen<SRC_KEYS>(root_seed, draws, m, n, t, rows, bits, stream);
+}
+
+extern "C" int frr_regen_exact(const uint64_t* ranks, int64_t m, int n, int t, int8_t* rows, uint32_t* bits,
+                               void* stream) {
+    return launch_regen<SRC_RANKS>(0, ranks, m, n, t, rows, bits, stream);
+}
+
+extern "C" int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t, const double* y,
+                          const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream) {
+    return launch_dim<SRC_KEYS>(root_seed, draws, nullptr, m, n, t, y, obs_bits, a, b, match, stream);
+}
+
+extern "C" int frr_dim_exact(const uint64_t* ranks, int64_t m, int n, int t, const double* y,
+                             const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream) {
+    return launch_dim<SRC_RANKS>(0, ranks, nullptr, m, n, t, y, obs_bits, a, b, match, stream);
+}
+
+extern "C" int frr_dim_rows(const int8_t* rows, int64_t m, int n, int t, const double* y,
+                            const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream) {
+    return launch_dim<SRC_ROWS>(0, nullptr, rows, m, n, t, y, obs_bits, a, b, match, stream);
+}
+
+extern "C" int frr_tau_counts(const double* a, const double* b, int64_t m, const double* taus, const double* rhs,
+                              int ntau, uint64_t* counts, void* stream) {
+    if (ntau <= 0) return FRR_OK;
+    cudaStream_t s = frr_stream(stream);
+    if (cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (size_t)ntau, s) != cudaSuccess)
+        return frr_check_launch("frr_tau_counts memset");
+    if (m <= 0) return FRR_OK;
+    int tiles = (ntau + kTauTile - 1) / kTauTile;
+    int64_t per_tile = std::max<int64_t>(1, (int64_t)frr_num_sms() * 8 / tiles);
+    per_tile = std::min<int64_t>(per_tile, frr_cdiv(m, 256));
+    dim3 grid((unsigned)per_tile, (unsigned)tiles);
+    k_tau_counts<<<grid, 256, 0, s>>>(a, b, m, taus, rhs, ntau, reinterpret_cast<unsigned long long*>(counts));
+    return frr_check_launch("k_tau_counts");
+}

@@ -1,0 +1,543 @@
+// frr_mma.cu -- fused Monte Carlo generation + tensor-core balance check.
+//
+// Replaces generation.py:185-204 (_pass1_stats) = keys.py:177-208 feeding
+// balance.py:93-105 for mid-size d.  Per 128-candidate tile:
+//
+//   FY warps (10)   key -> assignment in a per-warp smem table (frr_warp_fy),
+//                   packed to a bit row of the tile (never leaves the SM)
+//   tile warps (4)  expand bit rows to int8 0/1 A-operand K-chunks in the
+//                   tcgen05 K-major canonical layout; later the epilogue
+//   TMA warp        cp.async.bulk of the pre-tiled int8-limb B operand
+//                   (Zq split into L balanced base-256 digits, N = L*dpad)
+//   MMA warp        tcgen05.mma.cta_group::1.kind::i8, int32 accumulators
+//                   in TMEM (128 lanes x N columns)
+//   epilogue        tcgen05.ld, S_j = sum_l acc_l * 256^l (exact int64),
+//                   fp64 delta^2 with numpy's pairwise order, * const
+//
+// S = W . Zq is exact in every limb (|acc| <= 128 n < 2^31), so the
+// statistic is bit-identical to the reference's float64 BLAS path.
+#include <cuda_runtime.h>
+
+#include "frr_common.cuh"
+#include "frr_launch.cuh"
+
+namespace {
+
+constexpr int BM = 128;        // candidates per tile = MMA M
+constexpr int KC = 128;        // K bytes per pipeline stage
+constexpr int A_STAGES = 2;
+constexpr int B_STAGES = 2;
+constexpr int NFY = 10;        // generator warps
+constexpr int WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
+constexpr int NWARPS = WARP_FY0 + NFY;
+constexpr int NTHREADS = NWARPS * 32;
+constexpr int A_STAGE_BYTES = BM * KC;
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    const uint32_t a = smem_u32(b);
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, int32_t (&v)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, no swizzle (canonical layout
+// ((8,m),(T,2)):((1T,SBO),(1,LBO)) in 16-byte units).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // descriptor version (sm_100)
+    return d;         // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+}
+
+// instruction descriptor: kind::i8, D=s32, A=s8, B=s8, K-major both
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+struct MmaShape {
+    int n, t, d, L, dpad, npad, kpad, nkc, kw;  // kw: 32-bit words per bit row
+    int nparts, part_n[2], part_off[2];
+};
+
+__host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
+    MmaShape s;
+    s.n = n;
+    s.t = t;
+    s.d = d;
+    s.L = L;
+    s.dpad = (d + 15) & ~15;
+    s.npad = L * s.dpad;
+    s.kpad = (n + KC - 1) / KC * KC;
+    s.nkc = s.kpad / KC;
+    s.kw = s.kpad / 32;
+    s.nparts = s.npad > 256 ? 2 : 1;
+    // split N into <=256-column parts, each a multiple of 16
+    s.part_n[0] = s.nparts == 1 ? s.npad : ((s.npad / 2 + 15) & ~15);
+    s.part_n[1] = s.npad - s.part_n[0];
+    s.part_off[0] = 0;
+    s.part_off[1] = s.part_n[0];
+    return s;
+}
+
+struct SmemPlan {
+    size_t steps, tables, bits, a, b, bars, total;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
+    SmemPlan p;
+    size_t o = 0;
+    p.a = o;
+    o += (size_t)A_STAGES * A_STAGE_BYTES;
+    p.b = o;
+    o += (size_t)B_STAGES * s.npad * KC;
+    p.bits = o;
+    o += (size_t)2 * BM * (s.kw + 4) * 4;
+    p.steps = o;
+    o += align_up((size_t)s.t * sizeof(StepC), 16);
+    p.tables = o;
+    o += (size_t)NFY * frr_table_len(s.n) * 2;
+    o = align_up(o, 16);
+    p.bars = o;
+    o += 16 * 8 + 16;
+    p.total = o + 1024;  // slack for base alignment
+    return p;
+}
+
+// barrier slots
+enum { BAR_BITS_FULL = 0, BAR_BITS_EMPTY = 2, BAR_A_FULL = 4, BAR_A_EMPTY = 6, BAR_B_FULL = 8, BAR_B_EMPTY = 10,
+       BAR_TMEM_FULL = 12, BAR_TMEM_EMPTY = 13 };
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_mc_stats_mma(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(smem_raw), 1024));
+    const MmaShape S = mma_shape(bal.n, bal.t, bal.d, bal.n_limbs);
+    const SmemPlan P = smem_plan(S);
+    unsigned char* sA = smem + P.a;
+    unsigned char* sB = smem + P.b;
+    uint32_t* sBits = reinterpret_cast<uint32_t*>(smem + P.bits);
+    StepC* steps = reinterpret_cast<StepC*>(smem + P.steps);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (count + BM - 1) / BM;
+    const int rowstride = S.kw + 4;  // words; +16 B breaks bank aliasing of rows
+
+    frr_fill_steps(steps, S.n, S.t);
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[BAR_BITS_FULL + 0], NFY);
+        mbar_init(&bars[BAR_BITS_FULL + 1], NFY);
+        mbar_init(&bars[BAR_BITS_EMPTY + 0], 4);
+        mbar_init(&bars[BAR_BITS_EMPTY + 1], 4);
+        for (int s = 0; s < A_STAGES; s++) {
+            mbar_init(&bars[BAR_A_FULL + s], 4);
+            mbar_init(&bars[BAR_A_EMPTY + s], 1);
+        }
+        for (int s = 0; s < B_STAGES; s++) {
+            mbar_init(&bars[BAR_B_FULL + s], 1);
+            mbar_init(&bars[BAR_B_EMPTY + s], 1);
+        }
+        mbar_init(&bars[BAR_TMEM_FULL], 1);
+        mbar_init(&bars[BAR_TMEM_EMPTY], 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    if (warp == WARP_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp >= WARP_FY0) {
+        // ===================================================== generators
+        const int fyw = warp - WARP_FY0;
+        uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
+        int i = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
+            const int buf = i & 1;
+            mbar_wait(&bars[BAR_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
+            for (int r = fyw; r < BM; r += NFY) {
+                const int64_t c = tile * BM + r;
+                uint32_t* row = tb + (size_t)r * rowstride;
+                if (c < count) {
+                    frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
+                    for (int w = 0; w < S.kw; w++) {
+                        int e = w * 32 + lane;
+                        uint32_t word = __ballot_sync(FRR_FULL, e < S.n && lw[e] != FRR_CTL);
+                        if (lane == (w & 31)) row[w] = word;
+                    }
+                } else {
+                    for (int w = lane; w < S.kw; w += 32) row[w] = 0;
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mbar_arrive(&bars[BAR_BITS_FULL + buf]);
+        }
+    } else if (warp < 4) {
+        // ============================================ expansion + epilogue
+        const int r = threadIdx.x;  // tile row == TMEM lane
+        const double g = bal.g, cst = bal.cst;
+        const int d = S.d, full = d - (d % 8);
+        int i = 0;
+        uint32_t astage = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
+            const int buf = i & 1;
+            mbar_wait(&bars[BAR_BITS_FULL + buf], (i >> 1) & 1);
+            const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
+            for (int kc = 0; kc < S.nkc; kc++, astage++) {
+                const int s = astage % A_STAGES;
+                mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1);
+                const uint4 wv = *reinterpret_cast<const uint4*>(row + kc * 4);
+                const uint32_t w4[4] = {wv.x, wv.y, wv.z, wv.w};
+                unsigned char* dst = sA + (size_t)s * A_STAGE_BYTES + (r >> 3) * 128 + (r & 7) * 16;
+#pragma unroll
+                for (int k16 = 0; k16 < KC / 16; k16++) {
+                    uint32_t h = (w4[k16 >> 1] >> ((k16 & 1) * 16)) & 0xFFFFu;
+                    uint4 o;
+                    o.x = ((h & 0xF) * 0x00204081u) & 0x01010101u;
+                    o.y = (((h >> 4) & 0xF) * 0x00204081u) & 0x01010101u;
+                    o.z = (((h >> 8) & 0xF) * 0x00204081u) & 0x01010101u;
+                    o.w = (((h >> 12) & 0xF) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(dst + (size_t)k16 * (BM / 8) * 128) = o;
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[BAR_A_FULL + s]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
+
+            // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
+            mbar_wait(&bars[BAR_TMEM_FULL], i & 1);
+            tc_fence_after();
+            const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
+            double racc[8], tq[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) racc[k] = tq[k] = 0.0;
+            for (int jb = 0; jb < S.dpad; jb += 8) {
+                int64_t Sj[8];
+                {
+                    int32_t v[8];
+                    tc_ld8(tl + (uint32_t)((S.L - 1) * S.dpad + jb), v);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 8; u++) Sj[u] = v[u];
+                }
+                for (int l = S.L - 2; l >= 0; l--) {
+                    int32_t v[8];
+                    tc_ld8(tl + (uint32_t)(l * S.dpad + jb), v);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 256 + v[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int j = jb + u;
+                    if (j < d) {
+                        double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), bal.cc[j]);
+                        double q = __dmul_rn(delta, delta);
+                        if (j < full) {
+                            racc[u] = j < 8 ? q : __dadd_rn(racc[u], q);
+                        } else {
+                            tq[u] = q;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[BAR_TMEM_EMPTY]);
+            double res;
+            const int tail = d - full;
+            if (d < 8) {
+                res = -0.0;
+            } else {
+                res = __dadd_rn(__dadd_rn(__dadd_rn(racc[0], racc[1]), __dadd_rn(racc[2], racc[3])),
+                                __dadd_rn(__dadd_rn(racc[4], racc[5]), __dadd_rn(racc[6], racc[7])));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (u < tail) res = __dadd_rn(res, tq[u]);
+            const int64_t c = tile * BM + r;
+            if (c < count) out[c] = __dmul_rn(__dadd_rn(0.0, res), cst);
+        }
+    } else if (warp == WARP_TMA) {
+        // ============================================== B operand producer
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)S.npad * KC;
+            uint32_t bstage = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int kc = 0; kc < S.nkc; kc++, bstage++) {
+                    const int s = bstage % B_STAGES;
+                    mbar_wait(&bars[BAR_B_EMPTY + s], ((bstage / B_STAGES) & 1) ^ 1);
+                    mbar_expect_tx(&bars[BAR_B_FULL + s], bytes);
+                    bulk_g2s(sB + (size_t)s * bytes, bal.limbs + (size_t)kc * bytes, bytes, &bars[BAR_B_FULL + s]);
+                }
+            }
+        }
+    } else if (warp == WARP_MMA) {
+        // ===================================================== MMA issuer
+        if (lane == 0) {
+            uint32_t stage = 0;
+            int i = 0;
+            const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(S.npad / 8) * 128;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
+                mbar_wait(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1);
+                tc_fence_after();
+                for (int kc = 0; kc < S.nkc; kc++, stage++) {
+                    const int sa = stage % A_STAGES, sb = stage % B_STAGES;
+                    mbar_wait(&bars[BAR_A_FULL + sa], (stage / A_STAGES) & 1);
+                    mbar_wait(&bars[BAR_B_FULL + sb], (stage / B_STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + (size_t)sa * A_STAGE_BYTES);
+                    const uint32_t b0 = smem_u32(sB + (size_t)sb * S.npad * KC);
+#pragma unroll
+                    for (int ks = 0; ks < KC / 32; ks++) {
+                        const uint64_t ad = umma_desc(a0 + ks * 2 * a_lbo, a_lbo, 128);
+                        for (int p = 0; p < S.nparts; p++) {
+                            const uint64_t bd =
+                                umma_desc(b0 + ks * 2 * b_lbo + (uint32_t)(S.part_off[p] / 8) * 128, b_lbo, 128);
+                            tc_mma_i8(tmem_base + (uint32_t)S.part_off[p], ad, bd, idesc_i8(BM, S.part_n[p]),
+                                      (kc | ks) != 0);
+                        }
+                    }
+                    tc_commit(&bars[BAR_A_EMPTY + sa]);
+                    tc_commit(&bars[BAR_B_EMPTY + sb]);
+                }
+                tc_commit(&bars[BAR_TMEM_FULL]);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == WARP_MMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+// ------------------------------------------------------ limb preparation
+__global__ void k_prepare_limbs(const int64_t* __restrict__ zq, MmaShape S, int8_t* __restrict__ limbs,
+                                int32_t* overflow) {
+    const int64_t total = (int64_t)S.kpad * S.npad;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t chunk = (int64_t)S.npad * KC;
+        int kc = (int)(o / chunk);
+        int rem = (int)(o % chunk);
+        int k16 = rem / (S.npad * 16);
+        int rem2 = rem % (S.npad * 16);
+        int n8 = rem2 / 128;
+        int rem3 = rem2 % 128;
+        int rr = rem3 / 16, kb = rem3 % 16;
+        int k = kc * KC + k16 * 16 + kb;
+        int nrow = n8 * 8 + rr;
+        int l = nrow / S.dpad, j = nrow % S.dpad;
+        int8_t v = 0;
+        if (k < S.n && j < S.d && l < S.L) {
+            int64_t z = zq[(size_t)k * S.d + j];
+            for (int q = 0; q <= l; q++) {
+                v = (int8_t)(z & 0xFF);
+                z = (z - v) >> 8;
+            }
+            if (l == S.L - 1 && z != 0) atomicExch(overflow, 1);
+        }
+        limbs[o] = v;
+    }
+}
+
+
+// ------------------------------------------------ descriptor self-test
+// D[128 x N] = A[128 x K] . B[N x K]^T with one CTA, through the same
+// descriptor/idesc/TMEM code as the fused kernel (variant 1 swaps LBO/SBO,
+// for diagnosing layout conventions on hardware).
+__global__ void __launch_bounds__(128) k_selftest_mma(const int8_t* A, const int8_t* B, int K, int N, int32_t* D,
+                                                     int variant) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(smem_raw), 1024));
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + (size_t)BM * K;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (size_t)N * K);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // canonical K-major layout: [k16][row8][8][16]
+    for (int o = threadIdx.x; o < BM * K; o += blockDim.x) {
+        int r = o / K, k = o % K;
+        sA[((size_t)(k / 16) * (BM / 8) + r / 8) * 128 + (r % 8) * 16 + k % 16] = (unsigned char)A[o];
+    }
+    for (int o = threadIdx.x; o < N * K; o += blockDim.x) {
+        int r = o / K, k = o % K;
+        sB[((size_t)(k / 16) * (N / 8) + r / 8) * 128 + (r % 8) * 16 + k % 16] = (unsigned char)B[o];
+    }
+    fence_proxy_async();
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(N / 8) * 128;
+        for (int ks = 0; ks < K / 32; ks++) {
+            uint64_t ad, bd;
+            if (variant == 0) {
+                ad = umma_desc(smem_u32(sA) + ks * 2 * a_lbo, a_lbo, 128);
+                bd = umma_desc(smem_u32(sB) + ks * 2 * b_lbo, b_lbo, 128);
+            } else {
+                ad = umma_desc(smem_u32(sA) + ks * 2 * a_lbo, 128, a_lbo);
+                bd = umma_desc(smem_u32(sB) + ks * 2 * b_lbo, 128, b_lbo);
+            }
+            tc_mma_i8(tmem, ad, bd, idesc_i8(BM, N), ks != 0);
+        }
+        tc_commit(bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    const int r = threadIdx.x;
+    for (int c = 0; c < N; c += 8) {
+        int32_t v[8];
+        tc_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+        tc_wait_ld();
+        for (int u = 0; u < 8; u++) D[(size_t)r * N + c + u] = v[u];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+    (void)lane;
+}
+
+}  // namespace
+
+bool frr_mma_supported(const frr_balance_t* bal) {
+    if (bal->d <= 16 || bal->n_limbs < 1 || bal->n_limbs > 8) return false;
+    if (bal->n < 2 || bal->n > FRR_MAX_UNITS || bal->t <= 0 || bal->t >= bal->n) return false;
+    MmaShape s = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
+    if (s.npad > 512) return false;
+    return smem_plan(s).total <= 227 * 1024;
+}
+
+extern "C" size_t frr_limbs_bytes(int n, int d, int n_limbs) {
+    MmaShape s = mma_shape(n, 1, d, n_limbs);
+    return (size_t)s.kpad * s.npad;
+}
+
+extern "C" int frr_prepare_limbs(const int64_t* zq, int n, int d, int n_limbs, int8_t* limbs, int32_t* overflow_dev,
+                                 void* stream) {
+    if (n_limbs < 1 || n_limbs > 8 || n < 2 || d < 1) {
+        frr_set_error("frr_prepare_limbs: bad shape n=%d d=%d limbs=%d", n, d, n_limbs);
+        return FRR_E_INVALID_DESIGN;
+    }
+    cudaStream_t s = frr_stream(stream);
+    if (cudaMemsetAsync(overflow_dev, 0, sizeof(int32_t), s) != cudaSuccess) return frr_check_launch("overflow memset");
+    MmaShape S = mma_shape(n, 1, d, n_limbs);
+    int64_t total = (int64_t)S.kpad * S.npad;
+    int grid = (int)std::min<int64_t>(frr_cdiv(total, 256), (int64_t)frr_num_sms() * 16);
+    k_prepare_limbs<<<grid, 256, 0, s>>>(zq, S, limbs, overflow_dev);
+    return frr_check_launch("k_prepare_limbs");
+}
+
+int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats,
+                     void* stream) {
+    if (count <= 0) return FRR_OK;
+    MmaShape S = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
+    SmemPlan P = smem_plan(S);
+    int rc = frr_prepare_kernel(k_mc_stats_mma, P.total);
+    if (rc) return rc;
+    int64_t ntiles = frr_cdiv(count, BM);
+    int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
+    k_mc_stats_mma<<<grid, NTHREADS, P.total, frr_stream(stream)>>>(*bal, seed, lo, count, stats);
+    return frr_check_launch("k_mc_stats_mma");
+}
+
+extern "C" int frr_mc_stats_tc(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
+                               double* stats, void* stream) {
+    if (!bal || !bal->limbs || !frr_mma_supported(bal)) {
+        frr_set_error("frr_mc_stats_tc: shape not supported by the tensor-core path");
+        return FRR_E_UNSUPPORTED;
+    }
+    return frr_mc_stats_mma(bal, root_seed, draw_lo, count, stats, stream);
+}
+
+extern "C" int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t* D, int variant,
+                                   void* stream) {
+    if (K % 32 || K > 512 || N % 16 || N < 16 || N > 256) {
+        frr_set_error("selftest: K %% 32 == 0, K <= 512, N %% 16 == 0, 16 <= N <= 256");
+        return FRR_E_INVALID_DESIGN;
+    }
+    size_t smem = (size_t)BM * K + (size_t)N * K + 64 + 1024;
+    int rc = frr_prepare_kernel(k_selftest_mma, smem);
+    if (rc) return rc;
+    k_selftest_mma<<<1, 128, smem, frr_stream(stream)>>>(A, B, K, N, D, variant);
+    return frr_check_launch("k_selftest_mma");
+}

@@ -1,0 +1,275 @@
+// frr_select.cu -- exact k-smallest acceptance (generation.py:159-169).
+//
+// The reference stable-argsorts all M statistics (O(M log M) on the host).
+// Here: statistics are non-negative doubles, so their IEEE bit patterns
+// order like the values; an 8-pass, 8-bit MSD radix select finds the exact
+// threshold bit pattern T and the number of ties at T still to accept.  Ties
+// are accepted in index order, which is exactly the stable-argsort rule.  An
+// order-preserving compaction then emits the accepted indices ascending.
+// Multi-GPU: the per-pass histogram is all-reduced between frr_select_hist
+// and frr_select_pick; the tie quota is split by rank order on the host.
+#include <cuda_runtime.h>
+
+#include "frr_common.cuh"
+#include "frr_launch.cuh"
+
+namespace {
+
+constexpr int kHistThreads = 512;
+constexpr int kTile = 4096;  // compaction tile: 256 threads x 16 elements
+constexpr int kCThreads = 256;
+constexpr int kPer = kTile / kCThreads;
+
+__global__ void __launch_bounds__(kHistThreads) k_hist(const uint64_t* __restrict__ bits, int64_t m,
+                                                       const frr_select_state_t* st, int shift,
+                                                       unsigned long long* hist) {
+    __shared__ unsigned int sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint64_t prefix = st->prefix, mask = st->mask;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        bool ok = false;
+        unsigned digit = 0;
+        if (i < m) {
+            uint64_t v = bits[i];
+            ok = (v & mask) == prefix;
+            digit = (unsigned)(v >> shift) & 255u;
+        }
+        unsigned active = __ballot_sync(FRR_FULL, ok);
+        if (ok) {
+            // warp-aggregate equal digits: stats concentrate in few bins
+            unsigned peers = __match_any_sync(active, digit);
+            if ((__ffs(peers) - 1) == lane) atomicAdd(&sh[digit], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
+}
+
+__global__ void k_pick(const unsigned long long* hist, frr_select_state_t* st, int shift) {
+    if (threadIdx.x != 0) return;
+    int64_t k = st->k_rem;
+    unsigned long long cum = 0;
+    int digit = 255;
+    for (int dgt = 0; dgt < 256; dgt++) {
+        unsigned long long h = hist[dgt];
+        if ((int64_t)(cum + h) >= k) {
+            digit = dgt;
+            break;
+        }
+        cum += h;
+    }
+    st->k_rem = k - (int64_t)cum;
+    st->prefix |= (uint64_t)digit << shift;
+    st->mask |= 255ull << shift;
+}
+
+__global__ void k_init(frr_select_state_t* st, int64_t k) {
+    st->prefix = 0;
+    st->mask = 0;
+    st->k_rem = k;
+    st->pad = 0;
+}
+
+__global__ void __launch_bounds__(256) k_count(const uint64_t* __restrict__ bits, int64_t m,
+                                               const frr_select_state_t* st, unsigned long long* counts) {
+    const uint64_t T = st->prefix;
+    unsigned long long lt = 0, eq = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t v = bits[i];
+        lt += v < T;
+        eq += v == T;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lt += __shfl_xor_sync(FRR_FULL, lt, o);
+        eq += __shfl_xor_sync(FRR_FULL, eq, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lt) atomicAdd(counts, lt);
+        if (eq) atomicAdd(counts + 1, eq);
+    }
+}
+
+// per-tile (less, equal) counts
+__global__ void __launch_bounds__(kCThreads) k_tile_counts(const uint64_t* __restrict__ bits, int64_t m,
+                                                           const frr_select_state_t* st, int64_t* ws) {
+    const uint64_t T = st->prefix;
+    int64_t base = (int64_t)blockIdx.x * kTile;
+    int lt = 0, eq = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+        int64_t i = base + (int64_t)j * kCThreads + threadIdx.x;
+        if (i < m) {
+            uint64_t v = bits[i];
+            lt += v < T;
+            eq += v == T;
+        }
+    }
+    __shared__ int s_lt[kCThreads / 32], s_eq[kCThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        lt += __shfl_xor_sync(FRR_FULL, lt, o);
+        eq += __shfl_xor_sync(FRR_FULL, eq, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_lt[threadIdx.x >> 5] = lt;
+        s_eq[threadIdx.x >> 5] = eq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0, b = 0;
+        for (int w = 0; w < kCThreads / 32; w++) {
+            a += s_lt[w];
+            b += s_eq[w];
+        }
+        ws[2 * blockIdx.x] = a;
+        ws[2 * blockIdx.x + 1] = b;
+    }
+}
+
+// exclusive scan of the tile counts (single CTA), total accepted count
+__global__ void __launch_bounds__(1024) k_tile_scan(int64_t* ws, int64_t ntiles, const int64_t* tie_quota,
+                                                    int64_t* n_out) {
+    __shared__ int64_t s_a[1024], s_b[1024];
+    __shared__ int64_t carry_a, carry_b;
+    if (threadIdx.x == 0) carry_a = carry_b = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < ntiles; base += 1024) {
+        int64_t i = base + threadIdx.x;
+        int64_t a = i < ntiles ? ws[2 * i] : 0, b = i < ntiles ? ws[2 * i + 1] : 0;
+        s_a[threadIdx.x] = a;
+        s_b[threadIdx.x] = b;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            int64_t va = threadIdx.x >= o ? s_a[threadIdx.x - o] : 0;
+            int64_t vb = threadIdx.x >= o ? s_b[threadIdx.x - o] : 0;
+            __syncthreads();
+            s_a[threadIdx.x] += va;
+            s_b[threadIdx.x] += vb;
+            __syncthreads();
+        }
+        if (i < ntiles) {
+            ws[2 * i] = carry_a + s_a[threadIdx.x] - a;
+            ws[2 * i + 1] = carry_b + s_b[threadIdx.x] - b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            carry_a += s_a[1023];
+            carry_b += s_b[1023];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int64_t q = *tie_quota;
+        if (q > carry_b) q = carry_b;
+        if (q < 0) q = 0;
+        *n_out = carry_a + q;
+    }
+}
+
+__global__ void __launch_bounds__(kCThreads) k_compact(const uint64_t* __restrict__ bits, int64_t m, int64_t index_base,
+                                                       const frr_select_state_t* st, const int64_t* tie_quota,
+                                                       const int64_t* ws, int64_t* idx_out, double* stat_out) {
+    const uint64_t T = st->prefix;
+    const int64_t quota = *tie_quota;
+    int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;  // thread-contiguous run
+    uint64_t v[kPer];
+    int lt = 0, eq = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+        int64_t i = base + j;
+        v[j] = i < m ? bits[i] : ~0ull;
+        lt += v[j] < T;
+        eq += v[j] == T;
+    }
+    // block exclusive scan of (lt, eq) in thread order
+    __shared__ int s_lt[kCThreads], s_eq[kCThreads];
+    s_lt[threadIdx.x] = lt;
+    s_eq[threadIdx.x] = eq;
+    __syncthreads();
+    for (int o = 1; o < kCThreads; o <<= 1) {
+        int a = threadIdx.x >= o ? s_lt[threadIdx.x - o] : 0;
+        int b = threadIdx.x >= o ? s_eq[threadIdx.x - o] : 0;
+        __syncthreads();
+        s_lt[threadIdx.x] += a;
+        s_eq[threadIdx.x] += b;
+        __syncthreads();
+    }
+    int64_t lrank = ws[2 * blockIdx.x] + s_lt[threadIdx.x] - lt;
+    int64_t erank = ws[2 * blockIdx.x + 1] + s_eq[threadIdx.x] - eq;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+        bool less = v[j] < T, tie = v[j] == T;
+        if (less || (tie && erank < quota)) {
+            int64_t pos = lrank + (erank < quota ? erank : quota);
+            idx_out[pos] = index_base + base + j;
+            stat_out[pos] = __longlong_as_double((long long)v[j]);
+        }
+        lrank += less;
+        erank += tie;
+    }
+}
+
+}  // namespace
+
+extern "C" int frr_select_init(frr_select_state_t* st, int64_t k, void* stream) {
+    k_init<<<1, 1, 0, frr_stream(stream)>>>(st, k);
+    return frr_check_launch("k_init");
+}
+
+extern "C" int frr_select_hist(const double* stats, int64_t m, const frr_select_state_t* st, int pass,
+                               uint64_t* hist, void* stream) {
+    if (pass < 0 || pass > 7) {
+        frr_set_error("select pass %d outside [0, 7]", pass);
+        return FRR_E_INVALID_DESIGN;
+    }
+    cudaStream_t s = frr_stream(stream);
+    if (cudaMemsetAsync(hist, 0, 256 * sizeof(uint64_t), s) != cudaSuccess) return frr_check_launch("hist memset");
+    if (m <= 0) return FRR_OK;
+    int grid = (int)std::min<int64_t>(frr_cdiv(m, kHistThreads), (int64_t)frr_num_sms() * 4);
+    k_hist<<<grid, kHistThreads, 0, s>>>(reinterpret_cast<const uint64_t*>(stats), m, st, 56 - 8 * pass,
+                                         reinterpret_cast<unsigned long long*>(hist));
+    return frr_check_launch("k_hist");
+}
+
+extern "C" int frr_select_pick(const uint64_t* hist, frr_select_state_t* st, int pass, void* stream) {
+    k_pick<<<1, 32, 0, frr_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(hist), st, 56 - 8 * pass);
+    return frr_check_launch("k_pick");
+}
+
+extern "C" int frr_select_count(const double* stats, int64_t m, const frr_select_state_t* st, int64_t* counts,
+                                void* stream) {
+    cudaStream_t s = frr_stream(stream);
+    if (cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), s) != cudaSuccess) return frr_check_launch("count memset");
+    if (m <= 0) return FRR_OK;
+    int grid = (int)std::min<int64_t>(frr_cdiv(m, 256), (int64_t)frr_num_sms() * 8);
+    k_count<<<grid, 256, 0, s>>>(reinterpret_cast<const uint64_t*>(stats), m, st,
+                                 reinterpret_cast<unsigned long long*>(counts));
+    return frr_check_launch("k_count");
+}
+
+extern "C" size_t frr_select_workspace_bytes(int64_t m) {
+    return (size_t)std::max<int64_t>(1, frr_cdiv(m, kTile)) * 2 * sizeof(int64_t);
+}
+
+extern "C" int frr_select_compact(const double* stats, int64_t m, int64_t index_base, const frr_select_state_t* st,
+                                  const int64_t* tie_quota, int64_t* idx_out, double* stat_out, int64_t* n_out,
+                                  void* workspace, void* stream) {
+    cudaStream_t s = frr_stream(stream);
+    int64_t ntiles = frr_cdiv(m, kTile);
+    if (m <= 0) {
+        if (cudaMemsetAsync(n_out, 0, sizeof(int64_t), s) != cudaSuccess) return frr_check_launch("n_out memset");
+        return FRR_OK;
+    }
+    int64_t* ws = reinterpret_cast<int64_t*>(workspace);
+    const uint64_t* bits = reinterpret_cast<const uint64_t*>(stats);
+    k_tile_counts<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, st, ws);
+    int rc = frr_check_launch("k_tile_counts");
+    if (rc) return rc;
+    k_tile_scan<<<1, 1024, 0, s>>>(ws, ntiles, tie_quota, n_out);
+    if ((rc = frr_check_launch("k_tile_scan"))) return rc;
+    k_compact<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, index_base, st, tie_quota, ws, idx_out, stat_out);
+    return frr_check_launch("k_compact");
+}
