@@ -55,18 +55,25 @@ __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s) {
     return (uint32_t)(hi >> 32);
 }
 
+// t real steps, padded to a multiple of 64 with harmless dummies (b = 2) so
+// the generator can draw two full rounds per iteration without bounds tests.
+__host__ __device__ __forceinline__ int frr_steps_len(int t) { return (t + 63) & ~63; }
+
 __device__ inline void frr_fill_steps(StepC* steps, int n, int t) {
-    for (int k = threadIdx.x; k < t; k += blockDim.x) steps[k] = frr_make_step(n, k);
+    for (int k = threadIdx.x; k < frr_steps_len(t); k += blockDim.x) steps[k] = frr_make_step(k < t ? n : k + 2, k);
 }
 
-// Table words needed per candidate: n uint16 entries padded to 8 (16 bytes).
-__host__ __device__ __forceinline__ int frr_table_len(int n) { return (n + 7) & ~7; }
+// Table entries per candidate: n uint16 entries padded to a multiple of 32
+// (whole 64-byte words for the packers); padding entries read as control.
+__host__ __device__ __forceinline__ int frr_table_len(int n) { return (n + 31) & ~31; }
 
 __device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, int lane) {
     uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
     uint4 q = make_uint4(w, w, w, w);
     int len = frr_table_len(n);
     for (int i = lane * 8; i < len; i += 256) *reinterpret_cast<uint4*>(lw + i) = q;
+    __syncwarp();
+    if (n + lane < len) lw[n + lane] = 0xFFFFu;
 }
 
 // ----------------------------------------------------------- warp generator
@@ -81,35 +88,51 @@ __device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, 
 // table: lw[p] = 1 + (last step k < p with r_k = p).  The final content of a
 // position p >= t is found by following lw links to a never-written position
 // (its original element); those t..n-1 contents are the control units.
+__device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uint32_t& hmax) {
+    const uint4 q = *reinterpret_cast<const uint4*>(sp);  // one LDS.128
+    StepC s;
+    s.b = q.x;
+    s.c2 = q.y;
+    s.M = ((uint64_t)q.w << 32) | q.z;
+    const uint64_t u = frr_mix64(x);
+    hmax = max(hmax, (uint32_t)(u >> 32));  // a rejection needs hi(u) == 0xFFFFFFFF
+    return frr_mod_step(u, s);
+}
+
 __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
                                             uint16_t* lw, int lane) {
     frr_table_fill(lw, n, 0, lane);
     __syncwarp();
-    bool flag = false;
-    uint64_t x = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
-    const uint64_t stride = 32ull * FRR_GOLDEN;
-    for (int base = 0; base < t; base += 32) {
-        int k = base + lane;
-        bool pend = false;
-        uint32_t r = 0;
-        if (k < t) {
-            uint64_t u = frr_mix64(x);
-            StepC s = steps[k];
-            flag |= ((uint32_t)(u >> 32) == 0xFFFFFFFFu);
-            uint32_t rem = frr_mod_step(u, s);
-            r = (uint32_t)k + rem;
-            pend = rem != 0;
-        }
-        x += stride;
-        // last writer wins: later rounds overwrite, ties inside a round are
-        // settled by re-reading until the largest k of the round holds r
-        while (__any_sync(FRR_FULL, pend)) {
-            if (pend) lw[r] = (uint16_t)(k + 1);
+    uint32_t hmax = 0;
+    // two rounds (64 steps) per iteration: independent draws for ILP; the
+    // second round's steps are all later than the first's, so its stores go
+    // after the first round's and one verify loop settles both.
+    uint64_t x0 = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
+    uint64_t x1 = x0 + 32ull * FRR_GOLDEN;
+    const uint64_t stride = 64ull * FRR_GOLDEN;
+    // (padding steps k >= t may raise a spurious flag: p ~ 2^-32, harmless)
+    for (int base = 0; base < t; base += 64) {
+        const int k0 = base + lane, k1 = k0 + 32;
+        const uint32_t d0 = frr_fy_draw(x0, steps + k0, hmax);
+        const uint32_t d1 = frr_fy_draw(x1, steps + k1, hmax);
+        const uint32_t r0 = (uint32_t)k0 + d0, r1 = (uint32_t)k1 + d1;
+        x0 += stride;
+        x1 += stride;
+        const uint32_t v0 = (uint32_t)k0 + 1, v1 = (uint32_t)k1 + 1;
+        // self-swaps (d == 0) change nothing; padding steps store nothing
+        uint32_t p0 = (d0 != 0) & (k0 < t), p1 = (d1 != 0) & (k1 < t);
+        if (p0) lw[r0] = (uint16_t)v0;
+        if (p1) lw[r1] = (uint16_t)v1;
+        for (;;) {
             __syncwarp();
-            if (pend) pend = lw[r] < (uint16_t)(k + 1);
-            __syncwarp();
+            if (p0) p0 = (uint32_t)lw[r0] < v0;
+            if (p1) p1 = (uint32_t)lw[r1] < v1;
+            if (!__any_sync(FRR_FULL, p0 | p1)) break;
+            if (p0) lw[r0] = (uint16_t)v0;
+            if (p1) lw[r1] = (uint16_t)v1;
         }
     }
+    const bool flag = hmax == 0xFFFFFFFFu;
     if (__any_sync(FRR_FULL, flag)) {
         // exact sequential restatement with rejection (keys.py:146-156)
         __syncwarp();
@@ -131,16 +154,59 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         }
         __syncwarp();
     }
-    for (int p = t + lane; p < n; p += 32) {
-        int q = p;
-        uint32_t v = lw[q];
-        while (v != 0) {
-            q = (int)v - 1;
-            v = lw[q];
+    // Each lane walks its positions p = t+lane, t+lane+32, ... one link per
+    // iteration (no per-position warp reconvergence).  Chains are disjoint
+    // and end at distinct roots, so marking a root never disturbs a walk.
+    {
+        int p = t + lane, q = p;
+        while (p < n) {
+            const uint32_t v = lw[q];
+            if (v == 0) {
+                lw[q] = FRR_CTL;
+                p += 32;
+                q = p;
+            } else {
+                q = (int)v - 1;
+            }
         }
-        lw[q] = FRR_CTL;  // each chain ends at its own root: no other lane reads it
     }
     __syncwarp();
+}
+
+// Packed treated bits of one 32-unit word for t < 32768 (step marks k+1 <
+// 2^15, so bit 15 of an entry is set exactly for control units).  Bit
+// position -> unit map (the tensor-core B operand uses the same order):
+// bit 15-i <- unit 32w+2i, bit 31-i <- unit 32w+2i+1, i = 0..15.
+__host__ __device__ __forceinline__ int frr_packed_unit(int w, int p) {
+    return p < 16 ? 32 * w + 2 * (15 - p) : 32 * w + 2 * (31 - p) + 1;
+}
+
+__device__ __forceinline__ uint32_t frr_pack_word(const uint16_t* lw, int w) {
+    const uint4* src = reinterpret_cast<const uint4*>(lw + 32 * w);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const int cc = (c + w) & 3;  // rotate 16-byte chunks: conflict-free across lanes
+        const uint4 v = src[cc];
+        const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int i = 4 * cc + j;  // component index (units 32w+2i, 32w+2i+1)
+            acc |= (~x[j] & 0x80008000u) >> i;
+        }
+    }
+    return acc;
+}
+
+// Packed treated bits of the table: word w (units 32w..32w+31) lands in
+// lane (w & 31)'s return slot for its words; one ballot per word.
+template <class Store>
+__device__ __forceinline__ void frr_table_bits(const uint16_t* lw, int n, int words, int lane, Store store) {
+    for (int w = 0; w < words; w++) {
+        const int e = w * 32 + lane;
+        const uint32_t word = __ballot_sync(FRR_FULL, e < n && lw[e] != FRR_CTL);
+        if (lane == (w & 31)) store(w, word);
+    }
 }
 
 // ---------------------------------------------------- exact (combinadic)

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) k_regen(uint64_t seed, const uint64_
                                                     int t, int8_t* rows, uint32_t* bits) {
     extern __shared__ __align__(16) unsigned char smem[];
     StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? t : 0;
+    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
     uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uin
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = bal.n, t = bal.t, d = bal.d;
     StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? t : 0;
+    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
     uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) k_stats_generic(frr_balance_t bal, u
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = bal.n, t = bal.t, d = bal.d;
     StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? t : 0;
+    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
     double* scratch = reinterpret_cast<double*>(steps + nsteps);
     uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (size_t)kWarps * d);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t*
     extern __shared__ __align__(16) unsigned char smem[];
     const int maxl = plan_max_leaves(n);
     StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? t : 0;
+    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
     double* leafres = reinterpret_cast<double*>(steps + nsteps);          // [kWarps][2][maxl]
     int* leaf_off = reinterpret_cast<int*>(leafres + (size_t)kWarps * 2 * maxl);
     int* leaf_len = leaf_off + maxl;
@@ -476,7 +476,7 @@ int launch_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n, int t, in
     int rc = check_nt(n, t);
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
-    size_t smem = (SRC == SRC_KEYS ? (size_t)t * sizeof(StepC) : 0) + table_bytes(n);
+    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0) + table_bytes(n);
     auto kern = k_regen<SRC>;
     if ((rc = frr_prepare_kernel(kern, smem))) return rc;
     int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(m, kWarps));
@@ -487,7 +487,7 @@ int launch_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n, int t, in
 template <int SRC, int D>
 int launch_small(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, const int8_t* rows, uint64_t lo,
                  int64_t count, double* out, void* stream) {
-    size_t smem = (SRC == SRC_KEYS ? (size_t)bal->t * sizeof(StepC) : 0) + table_bytes(bal->n);
+    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(bal->t) * sizeof(StepC) : 0) + table_bytes(bal->n);
     auto kern = k_stats_small<SRC, D>;
     int rc = frr_prepare_kernel(kern, smem);
     if (rc) return rc;
@@ -505,7 +505,7 @@ int launch_stats(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, c
     if (bal->d <= 4) return launch_small<SRC, 4>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 8) return launch_small<SRC, 8>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 16) return launch_small<SRC, 16>(bal, seed, ids, rows, lo, count, out, stream);
-    size_t smem = (SRC == SRC_KEYS ? (size_t)bal->t * sizeof(StepC) : 0) + (size_t)kWarps * bal->d * sizeof(double) +
+    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(bal->t) * sizeof(StepC) : 0) + (size_t)kWarps * bal->d * sizeof(double) +
                   table_bytes(bal->n);
     if (smem > 227 * 1024) {
         frr_set_error("generic balance kernel needs %zu B shared memory (d=%d, n=%d)", smem, bal->d, bal->n);
@@ -537,7 +537,7 @@ int launch_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows, int64_t m
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
     int maxl = plan_max_leaves(n);
-    size_t smem = (SRC == SRC_KEYS ? (size_t)t * sizeof(StepC) : 0) + (size_t)kWarps * 2 * maxl * sizeof(double) +
+    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0) + (size_t)kWarps * 2 * maxl * sizeof(double) +
                   2 * (size_t)maxl * sizeof(int) + (size_t)((2 * maxl + 7) & ~7) * sizeof(int16_t) +
                   table_bytes(n);
     if (smem > 227 * 1024) {

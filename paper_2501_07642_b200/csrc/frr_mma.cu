@@ -24,10 +24,22 @@
 namespace {
 
 constexpr int BM = 128;        // candidates per tile = MMA M
-constexpr int KC = 128;        // K bytes per pipeline stage
-constexpr int A_STAGES = 2;
-constexpr int B_STAGES = 2;
-constexpr int NFY = 10;        // generator warps
+#ifndef FRR_MMA_NFY
+#define FRR_MMA_NFY 26
+#endif
+#ifndef FRR_MMA_KC
+#define FRR_MMA_KC 64
+#endif
+#ifndef FRR_MMA_STAGES
+#define FRR_MMA_STAGES 3
+#endif
+#ifndef FRR_WAIT_HINT_NS
+#define FRR_WAIT_HINT_NS 0
+#endif
+constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
+constexpr int A_STAGES = FRR_MMA_STAGES;
+constexpr int B_STAGES = FRR_MMA_STAGES;
+constexpr int NFY = FRR_MMA_NFY;  // generator warps
 constexpr int WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
 constexpr int NWARPS = WARP_FY0 + NFY;
 constexpr int NTHREADS = NWARPS * 32;
@@ -46,10 +58,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware
+// (NANOSLEEP.SYNCS) until the phase completes instead of spinning on issue
+// slots the generator warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     uint32_t ok = 0;
     const uint32_t a = smem_u32(b);
     do {
+#if FRR_WAIT_HINT_NS > 0
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "r"(FRR_WAIT_HINT_NS)
+            : "memory");
+#else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -57,6 +81,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "=r"(ok)
             : "r"(a), "r"(parity)
             : "memory");
+#endif
     } while (!ok);
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -148,24 +173,30 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     p.bits = o;
     o += (size_t)2 * BM * (s.kw + 4) * 4;
     p.steps = o;
-    o += align_up((size_t)s.t * sizeof(StepC), 16);
+    o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
     p.tables = o;
     o += (size_t)NFY * frr_table_len(s.n) * 2;
     o = align_up(o, 16);
     p.bars = o;
-    o += 16 * 8 + 16;
+    o += 32 * 8 + 16;
     p.total = o + 1024;  // slack for base alignment
     return p;
 }
 
 // barrier slots
-enum { BAR_BITS_FULL = 0, BAR_BITS_EMPTY = 2, BAR_A_FULL = 4, BAR_A_EMPTY = 6, BAR_B_FULL = 8, BAR_B_EMPTY = 10,
-       BAR_TMEM_FULL = 12, BAR_TMEM_EMPTY = 13 };
+constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = 2;
+constexpr int BAR_A_FULL = 4, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
+constexpr int BAR_B_FULL = BAR_A_EMPTY + A_STAGES, BAR_B_EMPTY = BAR_B_FULL + B_STAGES;
+constexpr int BAR_TMEM_FULL = BAR_B_EMPTY + B_STAGES, BAR_TMEM_EMPTY = BAR_TMEM_FULL + 1;
+constexpr int N_BARS = BAR_TMEM_EMPTY + 1;
+static_assert(N_BARS <= 30, "barrier slots");
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_mc_stats_mma(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(smem_raw), 1024));
+    // keep the shared address space visible to the compiler (LDS/STS, not
+    // generic LD/ST): align by offsetting the __shared__ array itself
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const MmaShape S = mma_shape(bal.n, bal.t, bal.d, bal.n_limbs);
     const SmemPlan P = smem_plan(S);
     unsigned char* sA = smem + P.a;
@@ -174,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     StepC* steps = reinterpret_cast<StepC*>(smem + P.steps);
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
@@ -222,11 +253,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 uint32_t* row = tb + (size_t)r * rowstride;
                 if (c < count) {
                     frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
-                    for (int w = 0; w < S.kw; w++) {
-                        int e = w * 32 + lane;
-                        uint32_t word = __ballot_sync(FRR_FULL, e < S.n && lw[e] != FRR_CTL);
-                        if (lane == (w & 31)) row[w] = word;
-                    }
+                    const int tw = frr_table_len(S.n) / 32;
+                    for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
                 } else {
                     for (int w = lane; w < S.kw; w += 32) row[w] = 0;
                 }
@@ -248,12 +276,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
                 const int s = astage % A_STAGES;
                 mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1);
-                const uint4 wv = *reinterpret_cast<const uint4*>(row + kc * 4);
-                const uint32_t w4[4] = {wv.x, wv.y, wv.z, wv.w};
+                const uint32_t* src = row + kc * (KC / 32);
+                uint32_t wv[KC / 32];
+#pragma unroll
+                for (int q = 0; q < KC / 32; q++) wv[q] = src[q];
                 unsigned char* dst = sA + (size_t)s * A_STAGE_BYTES + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
                 for (int k16 = 0; k16 < KC / 16; k16++) {
-                    uint32_t h = (w4[k16 >> 1] >> ((k16 & 1) * 16)) & 0xFFFFu;
+                    uint32_t h = (wv[k16 >> 1] >> ((k16 & 1) * 16)) & 0xFFFFu;
                     uint4 o;
                     o.x = ((h & 0xF) * 0x00204081u) & 0x01010101u;
                     o.y = (((h >> 4) & 0xF) * 0x00204081u) & 0x01010101u;
@@ -391,7 +421,8 @@ __global__ void k_prepare_limbs(const int64_t* __restrict__ zq, MmaShape S, int8
         int n8 = rem2 / 128;
         int rem3 = rem2 % 128;
         int rr = rem3 / 16, kb = rem3 % 16;
-        int k = kc * KC + k16 * 16 + kb;
+        int kk = kc * KC + k16 * 16 + kb;      // K index = packed bit position
+        int k = frr_packed_unit(kk >> 5, kk & 31);  // unit behind that bit
         int nrow = n8 * 8 + rr;
         int l = nrow / S.dpad, j = nrow % S.dpad;
         int8_t v = 0;
@@ -415,7 +446,7 @@ __global__ void k_prepare_limbs(const int64_t* __restrict__ zq, MmaShape S, int8
 __global__ void __launch_bounds__(128) k_selftest_mma(const int8_t* A, const int8_t* B, int K, int N, int32_t* D,
                                                      int variant) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(smem_raw), 1024));
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = smem;
     unsigned char* sB = smem + (size_t)BM * K;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (size_t)N * K);
@@ -482,6 +513,7 @@ __global__ void __launch_bounds__(128) k_selftest_mma(const int8_t* A, const int
 bool frr_mma_supported(const frr_balance_t* bal) {
     if (bal->d <= 16 || bal->n_limbs < 1 || bal->n_limbs > 8) return false;
     if (bal->n < 2 || bal->n > FRR_MAX_UNITS || bal->t <= 0 || bal->t >= bal->n) return false;
+    if (bal->t >= 32768) return false;  // frr_pack_word reads control marks from bit 15
     MmaShape s = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
     if (s.npad > 512) return false;
     return smem_plan(s).total <= 227 * 1024;
