@@ -11,8 +11,64 @@
 
 namespace {
 
-constexpr int kWarps = 8;  // warps per CTA for the warp-per-candidate kernels
+constexpr int kWarps = 8;  // max warps per CTA for the warp-per-candidate kernels
 constexpr int kThreads = kWarps * 32;
+
+// Shared-memory plan of a warp-per-candidate kernel: the Fisher-Yates step
+// table (shared, or global when t is too large), fixed per-CTA bytes, and a
+// per-warp part (the candidate table + scratch).  Huge n gets fewer warps.
+struct WarpPlan {
+    int warps;
+    bool gsteps;
+    size_t smem;
+};
+
+WarpPlan plan_warps(int t, bool needs_steps, size_t fixed, size_t per_warp) {
+    const size_t cap = 227 * 1024 - 1024;
+    const size_t steps_b = needs_steps ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0;
+    for (int g = 0; g < 2; g++) {
+        const bool gsteps = g == 1;
+        if (gsteps && !needs_steps) break;
+        const size_t f = fixed + (gsteps ? 0 : steps_b);
+        if (f + per_warp > cap) continue;
+        const int w = (int)std::min<size_t>(kWarps, (cap - f) / per_warp);
+        if (!gsteps && needs_steps && w < 4) continue;
+        return {w, gsteps, f + (size_t)w * per_warp};
+    }
+    return {0, false, 0};
+}
+
+__global__ void k_fill_steps_global(StepC* steps, int n, int t) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < frr_steps_len(t); k += gridDim.x * blockDim.x)
+        steps[k] = frr_make_step(k < t ? n : k + 2, k);
+}
+
+// Step table in global memory for the large-t plans (stream-ordered scratch).
+struct GlobalSteps {
+    StepC* p = nullptr;
+    cudaStream_t s;
+    int init(int n, int t, cudaStream_t st) {
+        s = st;
+        if (cudaMallocAsync((void**)&p, (size_t)frr_steps_len(t) * sizeof(StepC), s) != cudaSuccess)
+            return frr_check_launch("cudaMallocAsync(steps)");
+        k_fill_steps_global<<<std::max(1, frr_steps_len(t) / 256), 256, 0, s>>>(p, n, t);
+        return frr_check_launch("k_fill_steps_global");
+    }
+    ~GlobalSteps() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+// per-CTA steps pointer: shared copy (filled here) or the global table
+template <bool GS>
+__device__ __forceinline__ const StepC* cta_steps(unsigned char*& cursor, const StepC* gsteps, int n, int t, bool keys) {
+    if (!keys) return nullptr;
+    if (GS) return gsteps;
+    StepC* s = reinterpret_cast<StepC*>(cursor);
+    cursor += (size_t)frr_steps_len(t) * sizeof(StepC);
+    frr_fill_steps(s, n, t);
+    return s;
+}
 
 enum Source { SRC_KEYS = 0, SRC_RANKS = 1, SRC_ROWS = 2 };
 
@@ -47,19 +103,18 @@ __device__ __forceinline__ uint32_t table_word(const uint16_t* lw, int n, int w)
 }
 
 // ------------------------------------------------------------- regeneration
-template <int SRC>
+template <int SRC, bool GS>
 __global__ void __launch_bounds__(kThreads) k_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n,
-                                                    int t, int8_t* rows, uint32_t* bits) {
+                                                    int t, int8_t* rows, uint32_t* bits, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
-    StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
-    uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* cursor = smem;
+    const StepC* steps = cta_steps<GS>(cursor, gsteps, n, t, SRC == SRC_KEYS);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(cursor);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
-    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
     __syncthreads();
     const int words = (n + 31) >> 5;
-    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < m; c += (int64_t)gridDim.x * kWarps) {
+    for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < m; c += (int64_t)gridDim.x * nw) {
         build_table<SRC>(seed, ids, nullptr, c, n, t, steps, lw, lane);
         if (rows) {
             int8_t* out = rows + (size_t)c * n;
@@ -136,21 +191,20 @@ __device__ __forceinline__ void warp_sum(int64_t (&a)[D]) {
 // ------------------------------------------------ small-d balance (d <= 16)
 // S = colsum - sum over control units of Zq rows (exact int64), warp
 // reduction, then the fp64 epilogue on lane 0.
-template <int SRC, int D>
+template <int SRC, int D, bool GS>
 __global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
                                                           const int8_t* rows, uint64_t lo, int64_t count,
-                                                          double* out) {
+                                                          double* out, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = bal.n, t = bal.t, d = bal.d;
-    StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
-    uint16_t* tables = reinterpret_cast<uint16_t*>(steps + nsteps);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* cursor = smem;
+    const StepC* steps = cta_steps<GS>(cursor, gsteps, n, t, SRC == SRC_KEYS);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(cursor);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
-    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
     __syncthreads();
     const int64_t* __restrict__ zq = bal.zq;
-    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < count; c += (int64_t)gridDim.x * kWarps) {
+    for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < count; c += (int64_t)gridDim.x * nw) {
         if (SRC == SRC_KEYS) {
             frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
         } else {
@@ -181,22 +235,21 @@ __global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uin
 // --------------------------------------------- generic balance (any d)
 // Lanes own columns j; S_j = colsum_j - sum_{control e} Zq[e][j]; q_j to a
 // per-warp scratch; lane 0 runs the exact numpy pairwise sum.
-template <int SRC>
+template <int SRC, bool GS>
 __global__ void __launch_bounds__(kThreads) k_stats_generic(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
                                                             const int8_t* rows, uint64_t lo, int64_t count,
-                                                            double* out) {
+                                                            double* out, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = bal.n, t = bal.t, d = bal.d;
-    StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
-    double* scratch = reinterpret_cast<double*>(steps + nsteps);
-    uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (size_t)kWarps * d);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* cursor = smem;
+    const StepC* steps = cta_steps<GS>(cursor, gsteps, n, t, SRC == SRC_KEYS);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double* scratch = reinterpret_cast<double*>(cursor);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (size_t)nw * d);
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
     double* q = scratch + (size_t)warp * d;
-    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
     __syncthreads();
-    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < count; c += (int64_t)gridDim.x * kWarps) {
+    for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < count; c += (int64_t)gridDim.x * nw) {
         if (SRC == SRC_KEYS) {
             frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
         } else {
@@ -334,24 +387,25 @@ __device__ void plan_build(PwPlan& P, int off, int len) {
 
 __host__ __device__ inline int plan_max_leaves(int n) { return n / 64 + 2; }
 
-template <int SRC>
+template <int SRC, bool GS>
 __global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows,
                                                   int64_t m, int n, int t, const double* __restrict__ y,
                                                   const uint32_t* __restrict__ obs, double* a, double* b,
-                                                  int32_t* match) {
+                                                  int32_t* match, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int maxl = plan_max_leaves(n);
-    StepC* steps = reinterpret_cast<StepC*>(smem);
-    int nsteps = SRC == SRC_KEYS ? frr_steps_len(t) : 0;
-    double* leafres = reinterpret_cast<double*>(steps + nsteps);          // [kWarps][2][maxl]
-    int* leaf_off = reinterpret_cast<int*>(leafres + (size_t)kWarps * 2 * maxl);
+    unsigned char* cursor = smem;
+    const StepC* steps = cta_steps<GS>(cursor, gsteps, n, t, SRC == SRC_KEYS);
+    const int nw = blockDim.x >> 5;
+    double* leafres = reinterpret_cast<double*>(cursor);                   // [nw][2][maxl]
+    int* leaf_off = reinterpret_cast<int*>(leafres + (size_t)nw * 2 * maxl);
     int* leaf_len = leaf_off + maxl;
     int16_t* tok = reinterpret_cast<int16_t*>(leaf_len + maxl);          // [2*maxl]
     __shared__ int s_nleaf, s_ntok;
-    uint16_t* tables = reinterpret_cast<uint16_t*>(tok + ((2 * maxl + 7) & ~7));
+    size_t toff = reinterpret_cast<unsigned char*>(tok + ((2 * maxl + 7) & ~7)) - smem;
+    uint16_t* tables = reinterpret_cast<uint16_t*>(smem + ((toff + 15) & ~(size_t)15));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
-    if (SRC == SRC_KEYS) frr_fill_steps(steps, n, t);
     if (threadIdx.x == 0) {
         PwPlan P{0, 0, leaf_off, leaf_len, tok};
         plan_build(P, 0, n);
@@ -364,7 +418,7 @@ __global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t*
     double* rc = rt + maxl;
     const int words = (n + 31) >> 5;
     const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
-    for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < m; c += (int64_t)gridDim.x * kWarps) {
+    for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < m; c += (int64_t)gridDim.x * nw) {
         build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
         // b and membership from packed words
         uint32_t pt = 0, pc = 0;
@@ -456,7 +510,7 @@ __global__ void __launch_bounds__(256) k_tau_counts(const double* __restrict__ a
 }
 
 // -------------------------------------------------------- host helpers
-size_t table_bytes(int n) { return (size_t)kWarps * frr_table_len(n) * sizeof(uint16_t); }
+size_t table_bytes1(int n) { return (size_t)frr_table_len(n) * sizeof(uint16_t); }
 
 int check_nt(int n, int t) {
     if (n < 2 || n > FRR_MAX_UNITS) {
@@ -470,30 +524,50 @@ int check_nt(int n, int t) {
     return FRR_OK;
 }
 
+// Launch a warp-per-candidate kernel instantiated for shared (GS=false) or
+// global (GS=true) step tables according to the plan.
+template <class KS, class KG, class... Args>
+int launch_planned(const char* what, KS ks, KG kg, const WarpPlan& P, int n, int t, bool keys, int64_t items,
+                   void* stream, Args... args) {
+    if (P.warps < 1) {
+        frr_set_error("%s: n=%d does not fit shared memory", what, n);
+        return FRR_E_UNSUPPORTED;
+    }
+    cudaStream_t s = frr_stream(stream);
+    GlobalSteps gs;
+    int rc;
+    const int threads = P.warps * 32;
+    if (P.gsteps) {
+        if ((rc = gs.init(n, t, s))) return rc;
+        if ((rc = frr_prepare_kernel(kg, P.smem))) return rc;
+        int grid = frr_persistent_grid(kg, threads, P.smem, frr_cdiv(items, P.warps));
+        kg<<<grid, threads, P.smem, s>>>(args..., gs.p);
+    } else {
+        if ((rc = frr_prepare_kernel(ks, P.smem))) return rc;
+        int grid = frr_persistent_grid(ks, threads, P.smem, frr_cdiv(items, P.warps));
+        ks<<<grid, threads, P.smem, s>>>(args..., (const StepC*)nullptr);
+    }
+    (void)keys;
+    return frr_check_launch(what);
+}
+
 template <int SRC>
 int launch_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n, int t, int8_t* rows, uint32_t* bits,
                  void* stream) {
     int rc = check_nt(n, t);
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
-    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0) + table_bytes(n);
-    auto kern = k_regen<SRC>;
-    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
-    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(m, kWarps));
-    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(seed, ids, m, n, t, rows, bits);
-    return frr_check_launch("k_regen");
+    WarpPlan P = plan_warps(t, SRC == SRC_KEYS, 0, table_bytes1(n));
+    return launch_planned("k_regen", k_regen<SRC, false>, k_regen<SRC, true>, P, n, t, SRC == SRC_KEYS, m, stream,
+                          seed, ids, m, n, t, rows, bits);
 }
 
 template <int SRC, int D>
 int launch_small(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, const int8_t* rows, uint64_t lo,
                  int64_t count, double* out, void* stream) {
-    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(bal->t) * sizeof(StepC) : 0) + table_bytes(bal->n);
-    auto kern = k_stats_small<SRC, D>;
-    int rc = frr_prepare_kernel(kern, smem);
-    if (rc) return rc;
-    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, kWarps));
-    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, seed, ids, rows, lo, count, out);
-    return frr_check_launch("k_stats_small");
+    WarpPlan P = plan_warps(bal->t, SRC == SRC_KEYS, 0, table_bytes1(bal->n));
+    return launch_planned("k_stats_small", k_stats_small<SRC, D, false>, k_stats_small<SRC, D, true>, P, bal->n,
+                          bal->t, SRC == SRC_KEYS, count, stream, *bal, seed, ids, rows, lo, count, out);
 }
 
 template <int SRC>
@@ -505,17 +579,9 @@ int launch_stats(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, c
     if (bal->d <= 4) return launch_small<SRC, 4>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 8) return launch_small<SRC, 8>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 16) return launch_small<SRC, 16>(bal, seed, ids, rows, lo, count, out, stream);
-    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(bal->t) * sizeof(StepC) : 0) + (size_t)kWarps * bal->d * sizeof(double) +
-                  table_bytes(bal->n);
-    if (smem > 227 * 1024) {
-        frr_set_error("generic balance kernel needs %zu B shared memory (d=%d, n=%d)", smem, bal->d, bal->n);
-        return FRR_E_UNSUPPORTED;
-    }
-    auto kern = k_stats_generic<SRC>;
-    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
-    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, kWarps));
-    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, seed, ids, rows, lo, count, out);
-    return frr_check_launch("k_stats_generic");
+    WarpPlan P = plan_warps(bal->t, SRC == SRC_KEYS, 0, (size_t)bal->d * sizeof(double) + table_bytes1(bal->n));
+    return launch_planned("k_stats_generic", k_stats_generic<SRC, false>, k_stats_generic<SRC, true>, P, bal->n,
+                          bal->t, SRC == SRC_KEYS, count, stream, *bal, seed, ids, rows, lo, count, out);
 }
 
 template <int D>
@@ -537,18 +603,11 @@ int launch_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows, int64_t m
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
     int maxl = plan_max_leaves(n);
-    size_t smem = (SRC == SRC_KEYS ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0) + (size_t)kWarps * 2 * maxl * sizeof(double) +
-                  2 * (size_t)maxl * sizeof(int) + (size_t)((2 * maxl + 7) & ~7) * sizeof(int16_t) +
-                  table_bytes(n);
-    if (smem > 227 * 1024) {
-        frr_set_error("dim kernel needs %zu B shared memory (n=%d)", smem, n);
-        return FRR_E_UNSUPPORTED;
-    }
-    auto kern = k_dim<SRC>;
-    if ((rc = frr_prepare_kernel(kern, smem))) return rc;
-    int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(m, kWarps));
-    kern<<<grid, kThreads, smem, frr_stream(stream)>>>(seed, ids, rows, m, n, t, y, obs, a, b, match);
-    return frr_check_launch("k_dim");
+    size_t fixed = 2 * (size_t)maxl * sizeof(int) + (size_t)((2 * maxl + 7) & ~7) * sizeof(int16_t) + 16;
+    size_t per_warp = (size_t)2 * maxl * sizeof(double) + table_bytes1(n);
+    WarpPlan P = plan_warps(t, SRC == SRC_KEYS, fixed, per_warp);
+    return launch_planned("k_dim", k_dim<SRC, false>, k_dim<SRC, true>, P, n, t, SRC == SRC_KEYS, m, stream, seed,
+                          ids, rows, m, n, t, y, obs, a, b, match);
 }
 
 }  // namespace

@@ -1,0 +1,103 @@
+"""Multi-rank acceptance selection (NCCL on the GPU path) -- the host
+orchestration of _select.select_k_smallest run with world_size 2 over gloo
+on CPU.  The per-rank select steps are numpy restatements of the libfrr
+kernels (test-side checker ops); the orchestration under test is the
+product's: histogram all-reduce per radix pass, tie quota split in rank
+order, rank-ordered gather."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2501_07642_b200._select import TorchComm, select_k_smallest
+
+
+class NumpySelectOps:
+    def init(self, k, device):
+        return torch.tensor([0, 0, k, 0], dtype=torch.int64)
+
+    def _bits(self, stats):
+        return stats.numpy().view(np.uint64)
+
+    def hist(self, stats, st, p):
+        b = self._bits(stats)
+        prefix, mask = np.uint64(int(st[0]) & (2**64 - 1)), np.uint64(int(st[1]) & (2**64 - 1))
+        sel = b[(b & mask) == prefix]
+        digits = ((sel >> np.uint64(56 - 8 * p)) & np.uint64(255)).astype(np.int64)
+        return torch.from_numpy(np.bincount(digits, minlength=256).astype(np.int64))
+
+    def pick(self, hist, st, p):
+        k = int(st[2])
+        cum = np.cumsum(hist.numpy())
+        digit = int(np.searchsorted(cum, k))
+        before = int(cum[digit - 1]) if digit else 0
+        prefix = (int(st[0]) & (2**64 - 1)) | (digit << (56 - 8 * p))
+        mask = (int(st[1]) & (2**64 - 1)) | (255 << (56 - 8 * p))
+        st[0] = np.array([prefix], dtype=np.uint64).view(np.int64)[0]
+        st[1] = np.array([mask], dtype=np.uint64).view(np.int64)[0]
+        st[2] = k - before
+
+    def counts(self, stats, st):
+        b = self._bits(stats)
+        T = np.uint64(int(st[0]) & (2**64 - 1))
+        return torch.tensor([int((b < T).sum()), int((b == T).sum())], dtype=torch.int64)
+
+    def k_rem(self, st):
+        return st[2:3]
+
+    def compact(self, stats, index_base, st, quota, cap):
+        b = self._bits(stats)
+        T = np.uint64(int(st[0]) & (2**64 - 1))
+        q = int(quota.reshape(-1)[0])
+        eq_idx = np.flatnonzero(b == T)[: max(q, 0)]
+        idx = np.sort(np.concatenate([np.flatnonzero(b < T), eq_idx]))
+        return (torch.from_numpy(idx + index_base), stats[torch.from_numpy(idx)],
+                torch.tensor([idx.shape[0]], dtype=torch.int64))
+
+    def threshold(self, st):
+        return float(np.array([int(st[0]) & (2**64 - 1)], dtype=np.uint64).view(np.float64)[0])
+
+
+def _worker(rank, world, port, stats, p, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        M = stats.shape[0]
+        lo, hi = M * rank // world, M * (rank + 1) // world
+        k = max(1, math.floor(p * M))
+        idx, val, thr = select_k_smallest(torch.from_numpy(stats[lo:hi].copy()), lo, k, NumpySelectOps(),
+                                          TorchComm())
+        out[rank] = (idx.numpy(), val.numpy(), thr)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,ties,p", [(2, True, 0.1), (2, False, 0.01), (3, True, 0.37)])
+def test_distributed_select_matches_stable_sort(world, ties, p):
+    rng = np.random.default_rng(world * 7 + ties)
+    M = 20011
+    stats = np.round(rng.random(M) * (3 if ties else 1e6)) / 7.0
+    with mp.Manager() as man:
+        out = man.dict()
+        mp.spawn(_worker, args=(world, _free_port(), stats, p, out), nprocs=world, join=True)
+        results = dict(out)
+    k = max(1, math.floor(p * M))
+    order = np.argsort(stats, kind="stable")
+    want = np.sort(order[:k])
+    for r in range(world):
+        idx, val, thr = results[r]
+        assert np.array_equal(idx, want)
+        assert np.array_equal(val, stats[want])
+        assert thr == stats[order[k - 1]]

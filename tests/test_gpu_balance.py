@@ -1,0 +1,119 @@
+"""GPU balance statistics vs the reference's golden statistics and the C
+oracle -- bit-exact on every path (CUDA-core small-d, generic, tcgen05)."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2501_07642_b200 as frr
+from paper_2501_07642_b200 import _native as N
+from paper_2501_07642_b200 import generation as G
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1, 20, 5, "exact", 10), (2, 1000, 64, "exact", 500), (4, 34, 5, "exact", 17),
+          (100, 12, 3, "exact", 6), (108, 30, 40, "ridge", 15), (10, 16, 3, "diagonal", 5)]
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.asarray(a, dtype=np.float64).view(np.uint64), np.asarray(b, dtype=np.float64).view(np.uint64))
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"{s[1]}x{s[2]}{s[3]}")
+def test_golden_stats_rows_path(golden, shape):
+    seed, n, d, mode, t = shape
+    g = golden("balance")
+    tag = f"{seed}_{n}_{d}_{mode}"
+    X = np.random.default_rng(seed).standard_normal((n, d))
+    prec = frr.precompute_precision(X, mode)
+    want = g[f"stats_{tag}"]
+    W = frr.batch_assignments(seed, np.arange(want.shape[0], dtype=np.uint64), n, t)
+    assert bits_equal(frr.batch_balance(X, prec, W), want)
+    assert bits_equal(frr.batch_balance(X, prec, _mixed(n)), g[f"mixed_{tag}"])
+
+
+def _mixed(n):
+    W2 = np.zeros((8, n), dtype=np.int8)
+    for i in range(8):
+        W2[i, : 1 + (i * (n - 2)) // 7] = 1
+    return W2
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"{s[1]}x{s[2]}{s[3]}")
+@pytest.mark.parametrize("path", ["cuda_core", "tensor_core", "auto"])
+def test_golden_stats_mc_paths(golden, shape, path, monkeypatch):
+    seed, n, d, mode, t = shape
+    g = golden("balance")
+    want = g[f"stats_{seed}_{n}_{d}_{mode}"]
+    X = np.random.default_rng(seed).standard_normal((n, d))
+    kern = frr.precompute_precision(X, mode)._kernel
+    if path == "tensor_core" and d <= 16:
+        pytest.skip("tensor-core path is for d > 16")
+    monkeypatch.setenv("FRR_MC_PATH", path)
+    design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=want.shape[0], batch_size=1, root_seed=seed,
+                            precision_mode=mode)
+    st = G.mc_stats_device(kern, design, 0, want.shape[0]).cpu().numpy()
+    assert bits_equal(st, want)
+
+
+def test_hand_value():
+    X = np.array([[1.0], [2.0], [3.0], [4.0]])
+    st = frr.mahalanobis_stat(X, frr.precompute_precision(X, "exact"), np.array([1, 1, 0, 0], dtype=np.int8))
+    assert st == pytest.approx(2.4, rel=1e-9)
+
+
+# n spans the int8-limb counts (7 limbs n<=16, 6 limbs, 5 limbs n>4096)
+MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (300, 80, 150, "exact"),
+            (1000, 64, 500, "exact"), (1000, 64, 1, "exact"), (1000, 64, 999, "exact"), (2000, 70, 1000, "exact"),
+            (4500, 32, 2250, "exact"), (1000, 8, 500, "exact"), (5000, 3, 2500, "exact"), (200, 130, 100, "ridge")]
+
+
+@pytest.mark.parametrize("n,d,t,mode", MC_CASES)
+@pytest.mark.parametrize("path", ["auto", "cuda_core"])
+def test_mc_stats_vs_oracle(n, d, t, mode, path, monkeypatch):
+    X = np.random.default_rng(n * 31 + d).standard_normal((n, d)) * np.linspace(0.5, 3.0, d)
+    M = 3001 if n * max(d, 16) < 200_000 or path == "auto" else 300
+    monkeypatch.setenv("FRR_MC_PATH", path)
+    kern = frr.precompute_precision(X, mode)._kernel
+    design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=10**9, batch_size=1, root_seed=n + d + t,
+                            precision_mode=mode)
+    lo = 10**9 - M
+    st = G.mc_stats_device(kern, design, lo, M).cpu().numpy()
+    bal = O.Balance(kern._zq, kern._inv_scale_sq)
+    assert bits_equal(st, O.c_mc_stats(bal, t, design.root_seed, lo, M))
+
+
+@pytest.mark.parametrize("n,t,d", [(20, 10, 5), (34, 17, 5), (12, 6, 3), (26, 13, 16), (24, 12, 20), (64, 3, 4),
+                                   (80, 2, 5), (18, 9, 1)])
+def test_exact_stats_vs_oracle(n, t, d):
+    X = np.random.default_rng(n + d).standard_normal((n, d))
+    kern = frr.precompute_precision(X, "ridge")._kernel
+    total = math.comb(n, t)
+    lo = max(0, total - 250_000) if total > 500_000 else 0
+    design = frr.DesignSpec(n, t, accept_prob=1.0, mode="exact", enumeration_cap=10**12, precision_mode="ridge")
+    st = G.exact_stats_device(kern, design, lo, total - lo).cpu().numpy()
+    bal = O.Balance(kern._zq, kern._inv_scale_sq)
+    assert bits_equal(st, O.c_exact_stats(bal, t, lo, total - lo))
+
+
+@pytest.mark.parametrize("K,Nn", [(32, 16), (128, 64), (256, 192), (512, 256)])
+def test_tcgen05_selftest(K, Nn):
+    import torch
+
+    rng = np.random.default_rng(K + Nn)
+    A = (rng.random((128, K)) < 0.5).astype(np.int8)
+    B = rng.integers(-128, 128, size=(Nn, K)).astype(np.int8)
+    D = torch.zeros((128, Nn), dtype=torch.int32, device="cuda")
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    N.call("frr_selftest_mma_i8", N.ptr(dA), N.ptr(dB), K, Nn, N.ptr(D), 0, N.stream_ptr())
+    assert np.array_equal(D.cpu().numpy().astype(np.int64), A.astype(np.int64) @ B.astype(np.int64).T)
+
+
+def test_tensor_core_path_is_used_for_c2_shape():
+    X = np.random.default_rng(2).standard_normal((1000, 64))
+    kern = frr.precompute_precision(X, "exact")._kernel
+    os.environ.pop("FRR_MC_PATH", None)
+    assert kern.wants_tensor_cores() and kern.n_limbs == 6

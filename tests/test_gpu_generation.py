@@ -1,0 +1,188 @@
+"""GPU pool construction vs the reference's golden pools and the C oracle:
+accepted sets, statistics and thresholds bit-exact; size-independent
+properties at the full C2 size."""
+
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2501_07642_b200 as frr
+from paper_2501_07642_b200 import generation as G
+from paper_2501_07642_b200.errors import EnumerationTooLargeError, InvalidDesignError, StorageCapError
+
+pytestmark = pytest.mark.gpu
+
+
+def test_exact_pool_golden(golden):
+    g = golden("pools")
+    X = np.random.default_rng(102).standard_normal((10, 3))
+    pool = frr.enumerate_exact(X, frr.DesignSpec(10, 5, accept_prob=0.2, mode="exact"))
+    assert pool.n_candidates == 252 and pool.n_accepted == 50
+    assert np.array_equal(pool.accepted_indices, g["e10_acc"])
+    assert np.array_equal(pool.stats, g["e10_stats"]) and pool.threshold_value == float(g["e10_thr"])
+    assert np.array_equal(pool.assignments, g["e10_rows"])
+
+
+def test_c1_golden(golden):
+    g = golden("pools")
+    X = np.random.default_rng(1).standard_normal((20, 5))
+    pool = frr.generate_pool(X, frr.DesignSpec(20, 10, accept_prob=0.01, mode="exact", batch_size=10_000))
+    assert pool.n_candidates == 184_756 and pool.n_accepted == 1847
+    assert np.array_equal(pool.accepted_indices, g["c1_acc"]) and np.array_equal(pool.stats, g["c1_stats"])
+    assert pool.threshold_value == 0.7578915572820588
+
+
+MC = {
+    "mc12a": (100, (12, 3), dict(n_units=12, n_treated=6, accept_prob=0.05, max_draws=2000, batch_size=97, root_seed=21)),
+    "mc12all": (100, (12, 3), dict(n_units=12, n_treated=6, accept_prob=1.0, max_draws=2000, batch_size=2000, root_seed=21)),
+    "mc12one": (100, (12, 3), dict(n_units=12, n_treated=6, accept_prob=0.01, max_draws=100, batch_size=10, root_seed=9)),
+    "mctie": (None, (10, 1), dict(n_units=10, n_treated=5, accept_prob=0.02, max_draws=100, batch_size=25,
+                                  precision_mode="diagonal", root_seed=3)),
+    "mc20": (105, (20, 5), dict(n_units=20, n_treated=10, accept_prob=0.01, max_draws=100_000, batch_size=20_000,
+                                root_seed=12345)),
+    "mcridge": (108, (30, 40), dict(n_units=30, n_treated=15, accept_prob=0.1, max_draws=2000, batch_size=500,
+                                    precision_mode="ridge", root_seed=31)),
+    "mc1000": (2, (1000, 64), dict(n_units=1000, n_treated=500, accept_prob=1e-3, max_draws=20_000,
+                                   batch_size=10_000, root_seed=42)),
+}
+
+
+@pytest.mark.parametrize("name", list(MC))
+def test_mc_pools_golden(golden, name):
+    g = golden("pools")
+    xs, shape, kw = MC[name]
+    X = np.ones(shape) if xs is None else np.random.default_rng(xs).standard_normal(shape)
+    pool = frr.monte_carlo_pool(X, frr.DesignSpec(**kw))
+    assert np.array_equal(pool.accepted_indices, g[f"{name}_acc"])
+    assert np.array_equal(pool.stats, g[f"{name}_stats"]) and pool.threshold_value == float(g[f"{name}_thr"])
+    assert np.array_equal(pool.keys[:, 1], pool.accepted_indices.astype(np.uint64))
+
+
+def test_tie_break_by_draw_order():
+    pool = frr.monte_carlo_pool(np.ones((10, 1)), frr.DesignSpec(10, 5, accept_prob=0.02, max_draws=100,
+                                                                 batch_size=25, precision_mode="diagonal", root_seed=3))
+    assert pool.accepted_indices.tolist() == [0, 1] and pool.stats[0] == pool.stats[1]
+
+
+def test_batch_size_and_storage_invariance():
+    X = np.random.default_rng(100).standard_normal((12, 3))
+    base = frr.DesignSpec(12, 6, accept_prob=0.05, max_draws=2000, batch_size=2000, root_seed=21)
+    pools = [frr.monte_carlo_pool(X, dataclasses.replace(base, batch_size=b)) for b in (1, 7, 97, 2000)]
+    assert all(G.pools_equal(pools[0], p) for p in pools[1:])
+    full = frr.monte_carlo_pool(X, dataclasses.replace(base, storage="full"))
+    both = frr.monte_carlo_pool(X, dataclasses.replace(base, storage="both"))
+    regen = frr.regenerate_assignments(pools[0])
+    assert np.array_equal(regen, full.assignments) and np.array_equal(regen, both.assignments)
+    assert full.keys is None and both.keys is not None
+    prec = frr.precompute_precision(X, "exact")
+    assert np.array_equal(frr.batch_balance(X, prec, regen), pools[0].stats)
+    with pytest.raises(InvalidDesignError):
+        frr.regenerate_assignments(full)
+
+
+def test_acceptance_count_law():
+    X = np.random.default_rng(100).standard_normal((12, 3))
+    rng = np.random.default_rng(103)
+    for _ in range(10):
+        m = int(rng.integers(1, 2000))
+        p = float(rng.uniform(0.0005, 1.0))
+        pool = frr.monte_carlo_pool(X, frr.DesignSpec(12, 6, accept_prob=p, max_draws=m, batch_size=min(500, m),
+                                                      root_seed=int(rng.integers(0, 2**32))))
+        assert pool.n_accepted == max(1, math.floor(p * m))
+
+
+@pytest.mark.parametrize("M,p,ties", [(1, 1.0, False), (7, 1.0, True), (1000, 0.001, True), (100_003, 0.2, True),
+                                      (3_000_017, 1e-3, False), (2_000_000, 0.5, True)])
+def test_select_vs_oracle(M, p, ties):
+    rng = np.random.default_rng(M)
+    st = np.round(rng.random(M) * (5 if ties else 1e12)) / 3.0
+    st[: M // 10] = 0.0  # zeros (+0.0) sort first
+    acc, thr = G._select(st, p)
+    want, wthr = O.c_select(st, p)
+    assert np.array_equal(acc, want) and thr == wthr
+
+
+def test_c2_prefix_pool_vs_oracle():
+    X = np.random.default_rng(2).standard_normal((1000, 64))
+    design = frr.DesignSpec(1000, 500, accept_prob=1e-3, max_draws=200_000, batch_size=10_000, root_seed=42)
+    pool = frr.monte_carlo_pool(X, design)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    st = O.c_mc_stats(bal, 500, 42, 0, 200_000)
+    acc, thr = O.c_select(st, 1e-3)
+    assert np.array_equal(pool.accepted_indices, acc) and np.array_equal(pool.stats, st[acc])
+    assert pool.threshold_value == thr
+
+
+@pytest.mark.slow
+def test_c2_full_size_properties():
+    """Full C2 (1e8 candidates): accepted count, every accepted statistic
+    recomputed by the oracle bit-exactly, and 2e5 random candidates'
+    acceptance status consistent with the threshold."""
+    X = np.random.default_rng(2).standard_normal((1000, 64))
+    design = frr.DesignSpec(1000, 500, accept_prob=1e-3, max_draws=10**8, batch_size=10_000, root_seed=42)
+    pool = frr.monte_carlo_pool(X, design)
+    assert pool.n_accepted == 100_000
+    assert np.all(np.diff(pool.accepted_indices) > 0)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    sample = pool.accepted_indices[:: 10]
+    rows = O.c_batch_assign(42, sample.astype(np.uint64), 1000, 500)
+    assert np.array_equal(O.c_stats_rows(bal, rows, 500), pool.stats[:: 10])
+    assert pool.stats.max() == pool.threshold_value
+    rng = np.random.default_rng(9)
+    idx = np.unique(rng.integers(0, 10**8, size=200_000))
+    rows = O.c_batch_assign(42, idx.astype(np.uint64), 1000, 500)
+    st = O.c_stats_rows(bal, rows, 500)
+    accepted = np.isin(idx, pool.accepted_indices)
+    assert np.all(accepted[st < pool.threshold_value])
+    assert not np.any(accepted[st > pool.threshold_value])
+
+
+def test_exact_cap_and_storage_cap():
+    X = np.random.default_rng(106).standard_normal((20, 2))
+    with pytest.raises(EnumerationTooLargeError):
+        frr.enumerate_exact(X, frr.DesignSpec(20, 10, accept_prob=0.1, mode="exact", enumeration_cap=1000))
+    X12 = np.random.default_rng(100).standard_normal((12, 3))
+    with pytest.raises(StorageCapError):
+        frr.monte_carlo_pool(X12, frr.DesignSpec(12, 6, accept_prob=0.5, max_draws=1000, batch_size=100,
+                                                 storage="full", full_storage_cap=100))
+
+
+def test_pool_files_streaming_and_round_trip(tmp_path):
+    X = np.random.default_rng(100).standard_normal((12, 3))
+    base = frr.DesignSpec(12, 6, accept_prob=0.2, max_draws=300, batch_size=32, root_seed=19, storage="full")
+    streamed = tmp_path / "s.csv"
+    pool = frr.monte_carlo_pool(X, base, out_path=streamed)
+    assert pool.assignments is None
+    held = frr.monte_carlo_pool(X, base)
+    written = tmp_path / "h.csv"
+    frr.write_pool(held, written)
+    assert streamed.read_bytes() == written.read_bytes()
+    for storage in ("keys", "both"):
+        d = dataclasses.replace(base, storage=storage)
+        p = frr.monte_carlo_pool(X, d)
+        path = tmp_path / f"{storage}.csv"
+        frr.write_pool(p, path)
+        back = frr.read_pool(path)
+        assert np.array_equal(frr.pool_assignment_matrix(back), frr.pool_assignment_matrix(p))
+    Xe = np.random.default_rng(107).standard_normal((9, 2))
+    de = frr.DesignSpec(9, 4, accept_prob=0.3, mode="exact", batch_size=17)
+    a, b = tmp_path / "ea.csv", tmp_path / "eb.csv"
+    frr.enumerate_exact(Xe, de, out_path=a)
+    frr.write_pool(frr.enumerate_exact(Xe, de), b)
+    assert a.read_bytes() == b.read_bytes()
+
+
+def test_paper_api_generate_randomizations(tmp_path):
+    X = np.random.default_rng(3).standard_normal((20, 3))
+    r = frr.generate_randomizations(n_units=20, n_treated=10, X=X, randomization_accept_prob=0.01,
+                                    max_draws=10_000, batch_size=1000, randomization_type="monte_carlo", seed=5)
+    assert r.randomizations.shape == (100, 20) and np.array_equal(r.balance, r.stats)
+    e = frr.generate_randomizations(10, 5, np.random.default_rng(4).standard_normal((10, 3)),
+                                    randomization_type="exact", randomization_accept_prob=0.2)
+    assert e.randomizations.shape == (50, 10)
+    hi = frr.generate_randomizations(30, 15, np.random.default_rng(5).standard_normal((30, 40)),
+                                     max_draws=500, batch_size=500, approximate_inv=True)
+    assert hi.design.precision_mode == "ridge"
