@@ -12,6 +12,9 @@
 #define FRR_GOLDEN 0x9E3779B97F4A7C15ull
 #define FRR_FULL 0xffffffffu
 #define FRR_CTL 0xFFFFu  // table marker: unit is a control unit
+#ifndef FRR_FY_MATCH
+#define FRR_FY_MATCH 0
+#endif
 
 // ---------------------------------------------------------------- error state
 void frr_set_error(const char* fmt, ...);
@@ -49,18 +52,28 @@ __device__ __forceinline__ StepC frr_make_step(int n, int k) {
 }
 
 __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s) {
-    uint64_t y = (uint64_t)(uint32_t)(u >> 32) * s.c2 + (uint32_t)u;
-    uint64_t low = s.M * y;
-    uint64_t hi = (uint64_t)(uint32_t)(low >> 32) * s.b + __umulhi((uint32_t)low, s.b);
-    return (uint32_t)(hi >> 32);
+    // written on 32-bit halves so the result stays a plain 32-bit register
+    const uint32_t ulo = (uint32_t)u, uhi = (uint32_t)(u >> 32);
+    const uint32_t mlo = (uint32_t)s.M, mhi = (uint32_t)(s.M >> 32);
+    uint32_t ylo, yhi;  // y = uhi * c2 + ulo  (< 2^48)
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo));
+    // low = M * y mod 2^64
+    const uint32_t llo = mlo * ylo;
+    const uint32_t lhi = __umulhi(mlo, ylo) + mhi * ylo + mlo * yhi;
+    // result = floor(low * b / 2^64) = hi32(lhi * b + umulhi(llo, b))
+    uint32_t rlo, rhi;
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(rlo), "=r"(rhi) : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)));
+    (void)rlo;
+    return rhi;
 }
 
-// t real steps, padded to a multiple of 64 with harmless dummies (b = 2) so
-// the generator can draw two full rounds per iteration without bounds tests.
-__host__ __device__ __forceinline__ int frr_steps_len(int t) { return (t + 63) & ~63; }
+// t real steps, padded to a multiple of 64 with dummies of bound b = 1
+// (c2 = 0, M = 2^64 mod 2^64 = 0): frr_mod_step then returns 0, a self-swap
+// that stores nothing, so two full rounds per iteration need no bounds tests.
+__host__ __device__ __forceinline__ int frr_steps_len(int t) { return (t + 127) & ~127; }
 
 __device__ inline void frr_fill_steps(StepC* steps, int n, int t) {
-    for (int k = threadIdx.x; k < frr_steps_len(t); k += blockDim.x) steps[k] = frr_make_step(k < t ? n : k + 2, k);
+    for (int k = threadIdx.x; k < frr_steps_len(t); k += blockDim.x) steps[k] = frr_make_step(k < t ? n : k + 1, k);
 }
 
 // Table entries per candidate: n uint16 entries padded to a multiple of 32
@@ -99,39 +112,65 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
     return frr_mod_step(u, s);
 }
 
+#ifndef FRR_FY_ROUNDS
+#define FRR_FY_ROUNDS 2
+#endif
+#ifndef FRR_WALK_STREAMS
+#define FRR_WALK_STREAMS 1
+#endif
+
 __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
                                             uint16_t* lw, int lane) {
+    constexpr int R = FRR_FY_ROUNDS;
     frr_table_fill(lw, n, 0, lane);
     __syncwarp();
     uint32_t hmax = 0;
-    // two rounds (64 steps) per iteration: independent draws for ILP; the
-    // second round's steps are all later than the first's, so its stores go
-    // after the first round's and one verify loop settles both.
-    uint64_t x0 = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
-    uint64_t x1 = x0 + 32ull * FRR_GOLDEN;
-    const uint64_t stride = 64ull * FRR_GOLDEN;
-    // (padding steps k >= t may raise a spurious flag: p ~ 2^-32, harmless)
-    for (int base = 0; base < t; base += 64) {
-        const int k0 = base + lane, k1 = k0 + 32;
-        const uint32_t d0 = frr_fy_draw(x0, steps + k0, hmax);
-        const uint32_t d1 = frr_fy_draw(x1, steps + k1, hmax);
-        const uint32_t r0 = (uint32_t)k0 + d0, r1 = (uint32_t)k1 + d1;
-        x0 += stride;
-        x1 += stride;
-        const uint32_t v0 = (uint32_t)k0 + 1, v1 = (uint32_t)k1 + 1;
-        // self-swaps (d == 0) change nothing; padding steps store nothing
-        uint32_t p0 = (d0 != 0) & (k0 < t), p1 = (d1 != 0) & (k1 < t);
-        if (p0) lw[r0] = (uint16_t)v0;
-        if (p1) lw[r1] = (uint16_t)v1;
-        for (;;) {
+    // R rounds (32R steps) per iteration: independent draws for ILP; later
+    // rounds hold strictly later steps, so storing the rounds in order and
+    // settling them with one verify loop keeps "last writer wins".
+    uint64_t x[R];
+    x[0] = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
+#pragma unroll
+    for (int i = 1; i < R; i++) x[i] = x[i - 1] + 32ull * FRR_GOLDEN;
+    const uint64_t stride = 32ull * R * FRR_GOLDEN;
+    // (padding steps k >= t have b = 1: d = 0, no store; a spurious flag from
+    // them (p ~ 2^-32) only triggers the exact slow path)
+    for (int base = 0; base < t; base += 32 * R) {
+        uint32_t d[R], r[R], v[R], p[R];
+#pragma unroll
+        for (int i = 0; i < R; i++) {
+            const int k = base + 32 * i + lane;
+            d[i] = frr_fy_draw(x[i], steps + k, hmax);
+            r[i] = (uint32_t)k + d[i];
+            v[i] = (uint32_t)k + 1;
+            x[i] += stride;
+        }
+#pragma unroll
+        for (int i = 0; i < R; i++)
+            if (d[i] != 0) lw[r[i]] = (uint16_t)v[i];  // self-swaps change nothing
+        __syncwarp();
+        // a lower lane can lose a same-target race only to ... a lower lane:
+        // re-read (r is always a valid entry) and retry until settled
+        bool pend = false;
+#pragma unroll
+        for (int i = 0; i < R; i++) {
+            p[i] = (d[i] != 0) & ((uint32_t)lw[r[i]] < v[i]);
+            pend |= p[i] != 0;
+        }
+        while (__any_sync(FRR_FULL, pend)) {
+#pragma unroll
+            for (int i = 0; i < R; i++)
+                if (p[i]) lw[r[i]] = (uint16_t)v[i];
             __syncwarp();
-            if (p0) p0 = (uint32_t)lw[r0] < v0;
-            if (p1) p1 = (uint32_t)lw[r1] < v1;
-            if (!__any_sync(FRR_FULL, p0 | p1)) break;
-            if (p0) lw[r0] = (uint16_t)v0;
-            if (p1) lw[r1] = (uint16_t)v1;
+            pend = false;
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                if (p[i]) p[i] = (uint32_t)lw[r[i]] < v[i];
+                pend |= p[i] != 0;
+            }
         }
     }
+    __syncwarp();
     const bool flag = hmax == 0xFFFFFFFFu;
     if (__any_sync(FRR_FULL, flag)) {
         // exact sequential restatement with rejection (keys.py:146-156)
@@ -155,18 +194,33 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         __syncwarp();
     }
     // Each lane walks its positions p = t+lane, t+lane+32, ... one link per
-    // iteration (no per-position warp reconvergence).  Chains are disjoint
-    // and end at distinct roots, so marking a root never disturbs a walk.
+    // iteration, S interleaved walks for memory-level parallelism.  Chains
+    // are disjoint and end at distinct roots, so marking a root never
+    // disturbs another walk.
     {
-        int p = t + lane, q = p;
-        while (p < n) {
-            const uint32_t v = lw[q];
-            if (v == 0) {
-                lw[q] = FRR_CTL;
-                p += 32;
-                q = p;
-            } else {
-                q = (int)v - 1;
+        constexpr int S = FRR_WALK_STREAMS;
+        int pp[S], qq[S];
+#pragma unroll
+        for (int i = 0; i < S; i++) pp[i] = qq[i] = t + lane + 32 * i;
+        for (;;) {
+            bool live = false;
+#pragma unroll
+            for (int i = 0; i < S; i++) live |= pp[i] < n;
+            if (!live) break;
+            uint32_t vv[S];
+#pragma unroll
+            for (int i = 0; i < S; i++) vv[i] = pp[i] < n ? (uint32_t)lw[qq[i]] : 1u;
+#pragma unroll
+            for (int i = 0; i < S; i++) {
+                if (pp[i] < n) {
+                    if (vv[i] == 0) {
+                        lw[qq[i]] = FRR_CTL;
+                        pp[i] += 32 * S;
+                        qq[i] = pp[i];
+                    } else {
+                        qq[i] = (int)vv[i] - 1;
+                    }
+                }
             }
         }
     }

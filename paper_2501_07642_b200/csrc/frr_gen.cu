@@ -40,7 +40,7 @@ WarpPlan plan_warps(int t, bool needs_steps, size_t fixed, size_t per_warp) {
 
 __global__ void k_fill_steps_global(StepC* steps, int n, int t) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < frr_steps_len(t); k += gridDim.x * blockDim.x)
-        steps[k] = frr_make_step(k < t ? n : k + 2, k);
+        steps[k] = frr_make_step(k < t ? n : k + 1, k);
 }
 
 // Step table in global memory for the large-t plans (stream-ordered scratch).

@@ -33,6 +33,9 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_STAGES
 #define FRR_MMA_STAGES 3
 #endif
+#ifndef FRR_WAIT_SLEEP
+#define FRR_WAIT_SLEEP 0
+#endif
 #ifndef FRR_WAIT_HINT_NS
 #define FRR_WAIT_HINT_NS 0
 #endif
@@ -81,6 +84,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "=r"(ok)
             : "r"(a), "r"(parity)
             : "memory");
+#if FRR_WAIT_SLEEP > 0
+        if (!ok) __nanosleep(FRR_WAIT_SLEEP);  // back off: keep issue slots for the generators
+#endif
 #endif
     } while (!ok);
 }
