@@ -149,12 +149,12 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         for (int i = 0; i < R; i++)
             if (d[i] != 0) lw[r[i]] = (uint16_t)v[i];  // self-swaps change nothing
         __syncwarp();
-        // a lower lane can lose a same-target race only to ... a lower lane:
-        // re-read (r is always a valid entry) and retry until settled
+        // a higher lane's store can be overwritten by a lower lane's in the
+        // same instruction: re-read and retry until the largest k holds
         bool pend = false;
 #pragma unroll
         for (int i = 0; i < R; i++) {
-            p[i] = (d[i] != 0) & ((uint32_t)lw[r[i]] < v[i]);
+            p[i] = d[i] != 0 ? (uint32_t)lw[r[i]] < v[i] : 0u;  // r = k may lie past the table when d = 0
             pend |= p[i] != 0;
         }
         while (__any_sync(FRR_FULL, pend)) {

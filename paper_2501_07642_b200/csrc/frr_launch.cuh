@@ -45,3 +45,28 @@ static inline int frr_persistent_grid(K kernel, int threads, size_t smem, int64_
 }
 
 static inline cudaStream_t frr_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+namespace {
+__global__ void k_fill_steps_global(StepC* steps, int n, int t) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < frr_steps_len(t); k += gridDim.x * blockDim.x)
+        steps[k] = frr_make_step(k < t ? n : k + 1, k);
+}
+
+// Step table in global memory for the large-t plans (stream-ordered scratch).
+struct GlobalSteps {
+    StepC* p = nullptr;
+    cudaStream_t s;
+    int init(int n, int t, cudaStream_t st) {
+        s = st;
+        if (cudaMallocAsync((void**)&p, (size_t)frr_steps_len(t) * sizeof(StepC), s) != cudaSuccess)
+            return frr_check_launch("cudaMallocAsync(steps)");
+        k_fill_steps_global<<<std::max(1, frr_steps_len(t) / 256), 256, 0, s>>>(p, n, t);
+        return frr_check_launch("k_fill_steps_global");
+    }
+    ~GlobalSteps() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace
+

@@ -20,8 +20,10 @@
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
+#include "frr_tc.cuh"
 
 namespace {
+using namespace frr_tc;
 
 constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_NFY
@@ -33,12 +35,6 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_STAGES
 #define FRR_MMA_STAGES 3
 #endif
-#ifndef FRR_WAIT_SLEEP
-#define FRR_WAIT_SLEEP 0
-#endif
-#ifndef FRR_WAIT_HINT_NS
-#define FRR_WAIT_HINT_NS 0
-#endif
 constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
 constexpr int A_STAGES = FRR_MMA_STAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
@@ -47,96 +43,6 @@ constexpr int WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
 constexpr int NWARPS = WARP_FY0 + NFY;
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int A_STAGE_BYTES = BM * KC;
-
-// ------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-// try_wait with a suspend-time hint: a waiting warp sleeps in hardware
-// (NANOSLEEP.SYNCS) until the phase completes instead of spinning on issue
-// slots the generator warps need.
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    uint32_t ok = 0;
-    const uint32_t a = smem_u32(b);
-    do {
-#if FRR_WAIT_HINT_NS > 0
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity), "r"(FRR_WAIT_HINT_NS)
-            : "memory");
-#else
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-#if FRR_WAIT_SLEEP > 0
-        if (!ok) __nanosleep(FRR_WAIT_SLEEP);  // back off: keep issue slots for the generators
-#endif
-#endif
-    } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, int32_t (&v)[8]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// UMMA shared-memory descriptor, K-major, no swizzle (canonical layout
-// ((8,m),(T,2)):((1T,SBO),(1,LBO)) in 16-byte units).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= 1ull << 46;  // descriptor version (sm_100)
-    return d;         // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
-}
-
-// instruction descriptor: kind::i8, D=s32, A=s8, B=s8, K-major both
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
 
 struct MmaShape {
     int n, t, d, L, dpad, npad, kpad, nkc, kw;  // kw: 32-bit words per bit row
@@ -516,28 +422,56 @@ __global__ void __launch_bounds__(128) k_selftest_mma(const int8_t* A, const int
 
 }  // namespace
 
+// N-tiled variant for L*d beyond one TMEM accumulator (frr_mma_nt.cu)
+bool frr_nt_fits(int n, int d, int L);
+size_t frr_nt_limbs_bytes(int n, int d, int L);
+int frr_nt_prepare_limbs(const int64_t* zq, int n, int d, int L, int8_t* limbs, int32_t* overflow, cudaStream_t s);
+int frr_mc_stats_nt(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats,
+                    void* stream);
+
+namespace {
+enum TcLayout { TC_NONE = 0, TC_SINGLE = 1, TC_NT = 2 };
+
+// Which tensor-core kernel (and B-operand layout) serves (n, d, L).  Decided
+// without t (worst case t = n - 1) so the limb operand can be built once.
+TcLayout tc_layout(int n, int d, int L) {
+    if (d <= 16 || L < 1 || L > 8 || n < 2 || n > FRR_MAX_UNITS) return TC_NONE;
+    MmaShape s = mma_shape(n, n - 1, d, L);
+    if (s.npad <= 512 && smem_plan(s).total <= 227 * 1024) return TC_SINGLE;
+    if (frr_nt_fits(n, d, L)) return TC_NT;
+    return TC_NONE;
+}
+}  // namespace
+
 bool frr_mma_supported(const frr_balance_t* bal) {
-    if (bal->d <= 16 || bal->n_limbs < 1 || bal->n_limbs > 8) return false;
-    if (bal->n < 2 || bal->n > FRR_MAX_UNITS || bal->t <= 0 || bal->t >= bal->n) return false;
+    if (bal->t <= 0 || bal->t >= bal->n) return false;
     if (bal->t >= 32768) return false;  // frr_pack_word reads control marks from bit 15
-    MmaShape s = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
-    if (s.npad > 512) return false;
-    return smem_plan(s).total <= 227 * 1024;
+    return tc_layout(bal->n, bal->d, bal->n_limbs) != TC_NONE;
 }
 
 extern "C" size_t frr_limbs_bytes(int n, int d, int n_limbs) {
-    MmaShape s = mma_shape(n, 1, d, n_limbs);
-    return (size_t)s.kpad * s.npad;
+    switch (tc_layout(n, d, n_limbs)) {
+        case TC_SINGLE: {
+            MmaShape s = mma_shape(n, 1, d, n_limbs);
+            return (size_t)s.kpad * s.npad;
+        }
+        case TC_NT:
+            return frr_nt_limbs_bytes(n, d, n_limbs);
+        default:
+            return 0;
+    }
 }
 
 extern "C" int frr_prepare_limbs(const int64_t* zq, int n, int d, int n_limbs, int8_t* limbs, int32_t* overflow_dev,
                                  void* stream) {
-    if (n_limbs < 1 || n_limbs > 8 || n < 2 || d < 1) {
-        frr_set_error("frr_prepare_limbs: bad shape n=%d d=%d limbs=%d", n, d, n_limbs);
-        return FRR_E_INVALID_DESIGN;
+    const TcLayout lay = tc_layout(n, d, n_limbs);
+    if (lay == TC_NONE) {
+        frr_set_error("frr_prepare_limbs: no tensor-core layout for n=%d d=%d limbs=%d", n, d, n_limbs);
+        return FRR_E_UNSUPPORTED;
     }
     cudaStream_t s = frr_stream(stream);
     if (cudaMemsetAsync(overflow_dev, 0, sizeof(int32_t), s) != cudaSuccess) return frr_check_launch("overflow memset");
+    if (lay == TC_NT) return frr_nt_prepare_limbs(zq, n, d, n_limbs, limbs, overflow_dev, s);
     MmaShape S = mma_shape(n, 1, d, n_limbs);
     int64_t total = (int64_t)S.kpad * S.npad;
     int grid = (int)std::min<int64_t>(frr_cdiv(total, 256), (int64_t)frr_num_sms() * 16);
@@ -548,6 +482,7 @@ extern "C" int frr_prepare_limbs(const int64_t* zq, int n, int d, int n_limbs, i
 int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats,
                      void* stream) {
     if (count <= 0) return FRR_OK;
+    if (tc_layout(bal->n, bal->d, bal->n_limbs) == TC_NT) return frr_mc_stats_nt(bal, seed, lo, count, stats, stream);
     MmaShape S = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
     SmemPlan P = smem_plan(S);
     int rc = frr_prepare_kernel(k_mc_stats_mma, P.total);

@@ -68,7 +68,8 @@ def test_hand_value():
 # n spans the int8-limb counts (7 limbs n<=16, 6 limbs, 5 limbs n>4096)
 MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (300, 80, 150, "exact"),
             (1000, 64, 500, "exact"), (1000, 64, 1, "exact"), (1000, 64, 999, "exact"), (2000, 70, 1000, "exact"),
-            (4500, 32, 2250, "exact"), (1000, 8, 500, "exact"), (5000, 3, 2500, "exact"), (200, 130, 100, "ridge")]
+            (4500, 32, 2250, "exact"), (1000, 8, 500, "exact"), (5000, 3, 2500, "exact"), (200, 130, 100, "ridge"),
+            (2000, 1024, 1000, "ridge"), (1000, 1001, 17, "ridge"), (129, 300, 64, "diagonal")]
 
 
 @pytest.mark.parametrize("n,d,t,mode", MC_CASES)
@@ -76,6 +77,8 @@ MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (
 def test_mc_stats_vs_oracle(n, d, t, mode, path, monkeypatch):
     X = np.random.default_rng(n * 31 + d).standard_normal((n, d)) * np.linspace(0.5, 3.0, d)
     M = 3001 if n * max(d, 16) < 200_000 or path == "auto" else 300
+    if d > 200:
+        M = 1024 if path == "auto" else 64
     monkeypatch.setenv("FRR_MC_PATH", path)
     kern = frr.precompute_precision(X, mode)._kernel
     design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=10**9, batch_size=1, root_seed=n + d + t,

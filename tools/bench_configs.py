@@ -70,7 +70,7 @@ def c2():
             "tensor_TFLOPs_algorithmic": tf, "frac_of_bf16_sustained": tf / PEAKS.get("bf16_tflops_sustained", 1382.1)}
 
 
-def c3(M=4_000):
+def c3(M=2_000_000):
     X = np.random.default_rng(3).standard_normal((2000, 1024))
     design = frr.DesignSpec(2000, 1000, accept_prob=1e-4, max_draws=10**8, batch_size=10_000, root_seed=43,
                             precision_mode="ridge")

@@ -20,14 +20,19 @@ import paper_2501_07642_b200 as frr  # noqa: E402
 from paper_2501_07642_b200 import _native as N  # noqa: E402
 
 
+RESULTS = []
+
+
 def check(name, fn):
     t0 = time.time()
     try:
         ok, info = fn()
         torch.cuda.synchronize()
         print(f"[{'PASS' if ok else 'FAIL'}] {name}: {info} ({time.time() - t0:.2f}s)", flush=True)
+        RESULTS.append(ok)
     except Exception as exc:  # noqa: BLE001
         print(f"[ERROR] {name}: {exc!r}", flush=True)
+        RESULTS.append(False)
         traceback.print_exc()
 
 
@@ -149,6 +154,9 @@ if __name__ == "__main__":
     check("mc generic 30x40", lambda: mc_stats(30, 40, 15, 2000, "cuda_core", "ridge"))
     check("mc tc 30x40", lambda: mc_stats(30, 40, 15, 2000, "tensor_core", "ridge"))
     check("mc tc 1000x64", lambda: mc_stats(1000, 64, 500, 4096, "tensor_core"))
+    check("mc nt 2000x1024", lambda: mc_stats(2000, 1024, 1000, 2048, "tensor_core", "ridge"))
+    check("mc nt 300x200", lambda: mc_stats(300, 200, 150, 3000, "tensor_core", "ridge"))
+    check("mc nt 1000x1001", lambda: mc_stats(1000, 1001, 17, 1000, "tensor_core", "ridge"))
     check("exact 20/10/5", lambda: exact(20, 10, 5))
     check("exact 26/13/5", lambda: exact(26, 13, 5))
     check("exact 24/12/20", lambda: exact(24, 12, 20))
@@ -157,3 +165,4 @@ if __name__ == "__main__":
     check("C1 pool + test", c1_pool)
     check("t5k test path", t5k)
     check("bench mc 1000x64", bench_mc)
+    print(f"SUMMARY: {sum(RESULTS)}/{len(RESULTS)} passed", flush=True)
