@@ -235,6 +235,13 @@ __host__ __device__ __forceinline__ int frr_packed_unit(int w, int p) {
     return p < 16 ? 32 * w + 2 * (15 - p) : 32 * w + 2 * (31 - p) + 1;
 }
 
+// Tensor-core K order inside a packed word: K offset r (0..31) holds bit
+// 8*(r & 3) + (r >> 2), so the int8 0/1 expansion of bit word w is eight
+// registers ((w >> q) & 0x01010101), q = 0..7 (byte b of register q = K
+// offset 4q + b).  The B operand rows are permuted to the same order.
+__host__ __device__ __forceinline__ int frr_kpos_bit(int r) { return 8 * (r & 3) + (r >> 2); }
+__host__ __device__ __forceinline__ int frr_k_unit(int kk) { return frr_packed_unit(kk >> 5, frr_kpos_bit(kk & 31)); }
+
 __device__ __forceinline__ uint32_t frr_pack_word(const uint16_t* lw, int w) {
     const uint4* src = reinterpret_cast<const uint4*>(lw + 32 * w);
     uint32_t acc = 0;

@@ -195,12 +195,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 unsigned char* dst = sA + (size_t)s * A_STAGE_BYTES + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
                 for (int k16 = 0; k16 < KC / 16; k16++) {
-                    uint32_t h = (wv[k16 >> 1] >> ((k16 & 1) * 16)) & 0xFFFFu;
+                    // bytes 4j..4j+3 of this slab: (w >> (4*half + j)) & 0x01010101 (frr_kpos_bit order)
+                    const uint32_t w = wv[k16 >> 1];
+                    const int q0 = (k16 & 1) * 4;
                     uint4 o;
-                    o.x = ((h & 0xF) * 0x00204081u) & 0x01010101u;
-                    o.y = (((h >> 4) & 0xF) * 0x00204081u) & 0x01010101u;
-                    o.z = (((h >> 8) & 0xF) * 0x00204081u) & 0x01010101u;
-                    o.w = (((h >> 12) & 0xF) * 0x00204081u) & 0x01010101u;
+                    o.x = (w >> (q0 + 0)) & 0x01010101u;
+                    o.y = (w >> (q0 + 1)) & 0x01010101u;
+                    o.z = (w >> (q0 + 2)) & 0x01010101u;
+                    o.w = (w >> (q0 + 3)) & 0x01010101u;
                     *reinterpret_cast<uint4*>(dst + (size_t)k16 * (BM / 8) * 128) = o;
                 }
                 fence_proxy_async();
@@ -333,8 +335,8 @@ __global__ void k_prepare_limbs(const int64_t* __restrict__ zq, MmaShape S, int8
         int n8 = rem2 / 128;
         int rem3 = rem2 % 128;
         int rr = rem3 / 16, kb = rem3 % 16;
-        int kk = kc * KC + k16 * 16 + kb;      // K index = packed bit position
-        int k = frr_packed_unit(kk >> 5, kk & 31);  // unit behind that bit
+        int kk = kc * KC + k16 * 16 + kb;  // K index
+        int k = frr_k_unit(kk);             // unit behind that K position
         int nrow = n8 * 8 + rr;
         int l = nrow / S.dpad, j = nrow % S.dpad;
         int8_t v = 0;
@@ -386,18 +388,39 @@ __global__ void __launch_bounds__(128) k_selftest_mma(const int8_t* A, const int
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *slot;
+    const uint32_t a_tm = tmem + 256;  // variant 2: A staged in TMEM columns [256, 256 + K/4)
+    if (variant == 2) {
+        // row threadIdx.x -> TMEM lane, 4 consecutive K bytes per column
+        const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16) + 256;
+        for (int c0 = 0; c0 < K / 4; c0 += 32) {
+            uint32_t v[32];
+            for (int c = 0; c < 32; c++) {
+                uint32_t w = 0;
+                for (int b = 0; b < 4; b++) {
+                    const int k = (c0 + c) * 4 + b;
+                    w |= (k < K ? (uint32_t)(uint8_t)A[(size_t)threadIdx.x * K + k] : 0u) << (8 * b);
+                }
+                v[c] = w;
+            }
+            tc_st32(lane_base + (uint32_t)c0, v);
+        }
+        tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     if (threadIdx.x == 0) {
         const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(N / 8) * 128;
         for (int ks = 0; ks < K / 32; ks++) {
-            uint64_t ad, bd;
-            if (variant == 0) {
-                ad = umma_desc(smem_u32(sA) + ks * 2 * a_lbo, a_lbo, 128);
-                bd = umma_desc(smem_u32(sB) + ks * 2 * b_lbo, b_lbo, 128);
+            const uint64_t bd = variant == 1 ? umma_desc(smem_u32(sB) + ks * 2 * b_lbo, 128, b_lbo)
+                                             : umma_desc(smem_u32(sB) + ks * 2 * b_lbo, b_lbo, 128);
+            if (variant == 2) {
+                tc_mma_i8_ts(tmem, a_tm + (uint32_t)(ks * 8), bd, idesc_i8(BM, N), ks != 0);
             } else {
-                ad = umma_desc(smem_u32(sA) + ks * 2 * a_lbo, 128, a_lbo);
-                bd = umma_desc(smem_u32(sB) + ks * 2 * b_lbo, 128, b_lbo);
+                const uint64_t ad = variant == 1 ? umma_desc(smem_u32(sA) + ks * 2 * a_lbo, 128, a_lbo)
+                                                 : umma_desc(smem_u32(sA) + ks * 2 * a_lbo, a_lbo, 128);
+                tc_mma_i8(tmem, ad, bd, idesc_i8(BM, N), ks != 0);
             }
-            tc_mma_i8(tmem, ad, bd, idesc_i8(BM, N), ks != 0);
         }
         tc_commit(bar);
     }
@@ -504,8 +527,8 @@ extern "C" int frr_mc_stats_tc(const frr_balance_t* bal, uint64_t root_seed, uin
 
 extern "C" int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t* D, int variant,
                                    void* stream) {
-    if (K % 32 || K > 512 || N % 16 || N < 16 || N > 256) {
-        frr_set_error("selftest: K %% 32 == 0, K <= 512, N %% 16 == 0, 16 <= N <= 256");
+    if (K % 32 || K > 512 || N % 16 || N < 16 || N > 256 || (variant == 2 && (K > 1024 || K % 128))) {
+        frr_set_error("selftest: K %% 32 == 0, K <= 512, N %% 16 == 0, 16 <= N <= 256 (variant 2: K %% 128 == 0)");
         return FRR_E_INVALID_DESIGN;
     }
     size_t smem = (size_t)BM * K + (size_t)N * K + 64 + 1024;

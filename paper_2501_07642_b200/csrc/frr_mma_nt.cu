@@ -9,9 +9,12 @@
 // combine stack driven by a plan built once per CTA), so the statistic stays
 // bit-identical for any d.
 //
-// Warp roles (20 warps): 0-3 epilogue (TMEM lane quadrants), 4-7 A-operand
-// expansion (bit rows -> int8 K-chunks, once per N-chunk pass), 8 bulk copy of
-// the int8-limb B chunks, 9 tcgen05.mma issuer, 10-19 Fisher-Yates generators.
+// Warp roles: 0-3 epilogue (TMEM lane quadrants), 4-11 A-operand expansion
+// (bit rows -> int8 K-chunks written straight into TMEM with tcgen05.st, once
+// per N-chunk pass; the MMA reads A from TMEM, so only the B stream uses shared
+// memory bandwidth), then the bulk-copy warp for the int8-limb B chunks, the
+// tcgen05.mma issuer and the Fisher-Yates generator warps.
+// TMEM columns: [0, 2 NC) two accumulators, then a_st A stages of KC/4 columns.
 #include <cuda_runtime.h>
 
 #include "frr_common.cuh"
@@ -23,12 +26,22 @@ using namespace frr_tc;
 
 constexpr int BM = 128;
 constexpr int KC = 128;  // K bytes per stage
-constexpr int A_ST = 2, B_ST = 3;
-#ifndef FRR_NT_NFY
-#define FRR_NT_NFY 10
+#ifndef FRR_NT_AST
+#define FRR_NT_AST 3
 #endif
+#ifndef FRR_NT_NFY
+#define FRR_NT_NFY 8
+#endif
+#ifndef FRR_NT_NEXP
+#define FRR_NT_NEXP 8
+#endif
+#ifndef FRR_NT_BST
+#define FRR_NT_BST 4
+#endif
+constexpr int A_ST = FRR_NT_AST, B_ST = FRR_NT_BST;  // A stages live in TMEM (max A_ST)
 constexpr int NFY = FRR_NT_NFY;
-constexpr int W_EXP0 = 4, W_TMA = 8, W_MMA = 9, W_FY0 = 10;
+constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
+constexpr int W_EXP0 = 4, W_TMA = W_EXP0 + NEXP, W_MMA = W_TMA + 1, W_FY0 = W_MMA + 1;
 constexpr int NWARPS = W_FY0 + NFY;
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int DJ = 32;  // covariates per N-chunk
@@ -63,7 +76,6 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     NtPlan p;
     size_t o = 0;
     p.a = o;
-    o += (size_t)A_ST * BM * KC;
     p.b = o;
     o += (size_t)B_ST * s.nc * KC;
     p.bits = o;
@@ -104,6 +116,23 @@ __device__ void nt_build(int off, int len, uint32_t* starts, uint8_t* ncomb, int
     ncomb[nleaf - 1]++;
 }
 
+// wait with a short sleep between polls, for roles whose waits are long
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(128);
+    }
+}
+
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
     return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -116,7 +145,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const NtShape S = nt_shape(bal.n, bal.t, bal.d, bal.n_limbs);
     const NtPlan P = nt_plan(S);
-    unsigned char* sA = smem + P.a;
     unsigned char* sB = smem + P.b;
     uint32_t* sBits = reinterpret_cast<uint32_t*>(smem + P.bits);
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
@@ -127,6 +155,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
     const int rowstride = S.kw + 4;
+    const int a_st = min(A_ST, (512 - 2 * S.nc) / (KC / 4));  // A stages that fit in TMEM
 
     for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
     __syncthreads();
@@ -135,10 +164,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         nt_build(0, S.d, starts, ncomb, nleaf);
         mbar_init(&bars[B_BITS_FULL + 0], NFY);
         mbar_init(&bars[B_BITS_FULL + 1], NFY);
-        mbar_init(&bars[B_BITS_EMPTY + 0], 4);
-        mbar_init(&bars[B_BITS_EMPTY + 1], 4);
-        for (int s = 0; s < A_ST; s++) {
-            mbar_init(&bars[B_A_FULL + s], 4);
+        mbar_init(&bars[B_BITS_EMPTY + 0], NEXP);
+        mbar_init(&bars[B_BITS_EMPTY + 1], NEXP);
+        for (int s = 0; s < a_st; s++) {
+            mbar_init(&bars[B_A_FULL + s], NEXP);
             mbar_init(&bars[B_A_EMPTY + s], 1);
         }
         for (int s = 0; s < B_ST; s++) {
@@ -169,7 +198,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
-            mbar_wait(&bars[B_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
             for (int r = fyw; r < BM; r += NFY) {
                 const int64_t c = tile * BM + r;
@@ -184,36 +213,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (lane == 0) mbar_arrive(&bars[B_BITS_FULL + buf]);
         }
-    } else if (warp >= W_EXP0 && warp < W_EXP0 + 4) {
+    } else if (warp >= W_EXP0 && warp < W_EXP0 + NEXP) {
         // ============================ A expansion, once per N-chunk pass
-        const int r = threadIdx.x - W_EXP0 * 32;
+        constexpr int TPR = NEXP / 4;             // threads per row
+        constexpr int WPT = KC / 32 / TPR;        // bit words per thread per stage
+        static_assert(WPT == 2, "tcgen05.st.x16 covers 2 bit words");
+        const int et = threadIdx.x - W_EXP0 * 32;
+        const int r = et % BM, part = et / BM;   // r / 32 == warp % 4: this warp's TMEM lanes
+        const uint32_t lane_tm = tmem_base + ((uint32_t)((r >> 5) * 32) << 16) + (uint32_t)(2 * S.nc + part * 16);
         int i = 0;
-        uint32_t astage = 0;
+        int a_s = 0;
+        uint32_t a_ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
             mbar_wait(&bars[B_BITS_FULL + buf], (i >> 1) & 1);
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int c = 0; c < S.nch; c++) {
-                for (int kc = 0; kc < S.nkc; kc++, astage++) {
-                    const int s = astage % A_ST;
-                    mbar_wait(&bars[B_A_EMPTY + s], ((astage / A_ST) & 1) ^ 1);
-                    const uint32_t* src = row + kc * (KC / 32);
-                    unsigned char* dst = sA + (size_t)s * BM * KC + (r >> 3) * 128 + (r & 7) * 16;
+                for (int kc = 0; kc < S.nkc; kc++) {
+                    const int s = a_s;
+                    mbar_wait(&bars[B_A_EMPTY + s], a_ph ^ 1);
+                    if (++a_s == a_st) {
+                        a_s = 0;
+                        a_ph ^= 1;
+                    }
+                    tc_fence_after();
+                    const uint32_t* src = row + kc * (KC / 32) + part * WPT;
+                    uint32_t v[16];
 #pragma unroll
-                    for (int q = 0; q < KC / 32; q++) {
+                    for (int q = 0; q < WPT; q++) {
                         const uint32_t w = src[q];
 #pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            const uint32_t hw = (w >> (16 * h)) & 0xFFFFu;
-                            uint4 o;
-                            o.x = ((hw & 0xF) * 0x00204081u) & 0x01010101u;
-                            o.y = (((hw >> 4) & 0xF) * 0x00204081u) & 0x01010101u;
-                            o.z = (((hw >> 8) & 0xF) * 0x00204081u) & 0x01010101u;
-                            o.w = (((hw >> 12) & 0xF) * 0x00204081u) & 0x01010101u;
-                            *reinterpret_cast<uint4*>(dst + (size_t)(2 * q + h) * (BM / 8) * 128) = o;
-                        }
+                        for (int b = 0; b < 8; b++) v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
                     }
-                    fence_proxy_async();
+                    tc_st16(lane_tm + (uint32_t)(s * (KC / 4)), v);
+                    tc_wait_st();
+                    tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars[B_A_FULL + s]);
                 }
@@ -237,7 +271,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             bool done = false;
             for (int c = 0; c < S.nch; c++, chunk_ctr++) {
                 const int tb = chunk_ctr & 1;
-                mbar_wait(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1);
+                mbar_wait_lazy(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1);
                 tc_fence_after();
                 const uint32_t cb = tl + (uint32_t)(tb * S.nc);
                 for (int g4 = 0; g4 < DJ / 8; g4++) {
@@ -326,8 +360,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == W_MMA) {
         if (lane == 0) {
-            uint32_t stage = 0, chunk_ctr = 0;
-            const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(S.nc / 8) * 128;
+            uint32_t chunk_ctr = 0, m_aph = 0, m_bph = 0;
+            int m_as = 0, m_bs = 0;
+            const uint32_t b_lbo = (uint32_t)(S.nc / 8) * 128;
             const uint32_t idesc = idesc_i8(BM, S.nc);
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int c = 0; c < S.nch; c++, chunk_ctr++) {
@@ -335,17 +370,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_wait(&bars[B_TM_EMPTY + tb], ((chunk_ctr >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t dt = tmem_base + (uint32_t)(tb * S.nc);
-                    for (int kc = 0; kc < S.nkc; kc++, stage++) {
-                        const int sa = stage % A_ST, sb = stage % B_ST;
-                        mbar_wait(&bars[B_A_FULL + sa], (stage / A_ST) & 1);
-                        mbar_wait(&bars[B_B_FULL + sb], (stage / B_ST) & 1);
+                    for (int kc = 0; kc < S.nkc; kc++) {
+                        const int sa = m_as, sb = m_bs;
+                        mbar_wait(&bars[B_A_FULL + sa], m_aph);
+                        mbar_wait(&bars[B_B_FULL + sb], m_bph);
+                        if (++m_as == a_st) {
+                            m_as = 0;
+                            m_aph ^= 1;
+                        }
+                        if (++m_bs == B_ST) {
+                            m_bs = 0;
+                            m_bph ^= 1;
+                        }
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + (size_t)sa * BM * KC);
+                        const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + sa * (KC / 4));
                         const uint32_t b0 = smem_u32(sB + (size_t)sb * S.nc * KC);
 #pragma unroll
                         for (int ks = 0; ks < KC / 32; ks++) {
-                            tc_mma_i8(dt, umma_desc(a0 + ks * 2 * a_lbo, a_lbo, 128),
-                                      umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc, (kc | ks) != 0);
+                            tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc,
+                                         (kc | ks) != 0);
                         }
                         tc_commit(&bars[B_A_EMPTY + sa]);
                         tc_commit(&bars[B_B_EMPTY + sb]);
@@ -378,7 +421,7 @@ __global__ void k_prepare_limbs_nt(const int64_t* __restrict__ zq, NtShape S, in
         const int nrow = (rem2 / 128) * 8 + (rem2 % 128) / 16;
         const int kb = rem2 % 16;
         const int kk = kc * KC + k16 * 16 + kb;
-        const int k = frr_packed_unit(kk >> 5, kk & 31);
+        const int k = frr_k_unit(kk);
         const int l = nrow / DJ, j = c * DJ + nrow % DJ;
         int8_t v = 0;
         if (k < S.n && j < S.d && l < S.L) {
@@ -400,6 +443,7 @@ bool frr_nt_fits(int n, int d, int L) {
     if (d < 8 || L < 1 || L > 8 || n > FRR_MAX_UNITS) return false;
     NtShape s = nt_shape(n, n - 1, d, L);
     if (s.nc > 256 || s.dpad / 8 > 8 * MAX_LEAVES) return false;
+    if (2 * s.nc + 2 * (KC / 4) > 512) return false;  // two accumulators + >= 2 A stages in TMEM
     return nt_plan(s).total <= 227 * 1024;
 }
 

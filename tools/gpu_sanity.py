@@ -147,6 +147,8 @@ if __name__ == "__main__":
     print(torch.cuda.get_device_name(0), flush=True)
     check("mma selftest v0", lambda: selftest(0))
     check("mma selftest v0 K=256 N=192", lambda: selftest(0, 256, 192))
+    check("mma selftest A-in-TMEM K=128 N=64", lambda: selftest(2, 128, 64))
+    check("mma selftest A-in-TMEM K=256 N=192", lambda: selftest(2, 256, 192))
     for n, t in [(2, 1), (10, 7), (33, 16), (1000, 500), (5000, 2500)]:
         check(f"regen {n},{t}", lambda n=n, t=t: regen(n, t))
     check("mc small 20x5", lambda: mc_stats(20, 5, 10, 20000, "cuda_core"))
