@@ -35,6 +35,9 @@ constexpr int KC = 128;  // K bytes per stage
 #ifndef FRR_NT_NEXP
 #define FRR_NT_NEXP 8
 #endif
+#ifndef FRR_NT_HWWAIT
+#define FRR_NT_HWWAIT 0
+#endif
 #ifndef FRR_NT_BST
 #define FRR_NT_BST 4
 #endif
@@ -133,6 +136,25 @@ __device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity) {
     }
 }
 
+// hardware-suspended wait (try_wait with a time hint): no issue slots spent
+__device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
+#if FRR_NT_HWWAIT
+    const uint32_t a = smem_u32(b);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "r"(100000)
+            : "memory");
+    } while (!ok);
+#else
+    mbar_wait(b, parity);
+#endif
+}
+
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
     return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -226,12 +248,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t a_ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
-            mbar_wait(&bars[B_BITS_FULL + buf], (i >> 1) & 1);
+            mbar_wait_hw(&bars[B_BITS_FULL + buf], (i >> 1) & 1);
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int c = 0; c < S.nch; c++) {
                 for (int kc = 0; kc < S.nkc; kc++) {
                     const int s = a_s;
-                    mbar_wait(&bars[B_A_EMPTY + s], a_ph ^ 1);
+                    mbar_wait_hw(&bars[B_A_EMPTY + s], a_ph ^ 1);
                     if (++a_s == a_st) {
                         a_s = 0;
                         a_ph ^= 1;
@@ -350,7 +372,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int c = 0; c < S.nch; c++) {
                     for (int kc = 0; kc < S.nkc; kc++, bstage++) {
                         const int s = bstage % B_ST;
-                        mbar_wait(&bars[B_B_EMPTY + s], ((bstage / B_ST) & 1) ^ 1);
+                        mbar_wait_hw(&bars[B_B_EMPTY + s], ((bstage / B_ST) & 1) ^ 1);
                         mbar_expect_tx(&bars[B_B_FULL + s], bytes);
                         bulk_g2s(sB + (size_t)s * bytes, bal.limbs + ((size_t)c * S.nkc + kc) * bytes, bytes,
                                  &bars[B_B_FULL + s]);
