@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
-            mbar_wait(&bars[BAR_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
             for (int r = fyw; r < BM; r += NFY) {
                 const int64_t c = tile * BM + r;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t astage = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
-            mbar_wait(&bars[BAR_BITS_FULL + buf], (i >> 1) & 1);
+            mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i >> 1) & 1);
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
                 const int s = astage % A_STAGES;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
 
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
-            mbar_wait(&bars[BAR_TMEM_FULL], i & 1);
+            mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1);
             tc_fence_after();
             const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
             double racc[8], tq[8];
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kc = 0; kc < S.nkc; kc++, bstage++) {
                     const int s = bstage % B_STAGES;
-                    mbar_wait(&bars[BAR_B_EMPTY + s], ((bstage / B_STAGES) & 1) ^ 1);
+                    mbar_wait_long(&bars[BAR_B_EMPTY + s], ((bstage / B_STAGES) & 1) ^ 1);
                     mbar_expect_tx(&bars[BAR_B_FULL + s], bytes);
                     bulk_g2s(sB + (size_t)s * bytes, bal.limbs + (size_t)kc * bytes, bytes, &bars[BAR_B_FULL + s]);
                 }
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int i = 0;
             const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(S.npad / 8) * 128;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-                mbar_wait(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1);
+                mbar_wait_long(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1);
                 tc_fence_after();
                 for (int kc = 0; kc < S.nkc; kc++, stage++) {
                     const int sa = stage % A_STAGES, sb = stage % B_STAGES;
