@@ -27,7 +27,7 @@ from .errors import (
     InvalidDesignError,
     UnsupportedStatisticError,
 )
-from .generation import DesignSpec, RandomizationPool, generate_pool, pool_assignment_matrix
+from .generation import DesignSpec, RandomizationPool, pool_assignment_matrix
 from .keys import Assignment
 
 _BISECT_DEPTH = 6  # bisection levels evaluated per launch (2^6 - 1 taus)
@@ -364,14 +364,30 @@ def _observed_from_rule(rule, pool: RandomizationPool) -> np.ndarray:
 def threshold_sweep(X, base_design: DesignSpec, probs, obs_y, obs_w_rule="first", find_fi: bool = False,
                     alpha: float = 0.05, workers: int | None = None) -> list[dict]:
     """Pool + test per acceptance probability, same seed and draw count
-    (inference.py:279-312); failing rows are recorded and the sweep goes on."""
+    (inference.py:279-312); failing rows are recorded and the sweep goes on.
+
+    Candidate statistics do not depend on the acceptance probability, so
+    pass 1 (generation + balance check) runs once on the GPU and every row
+    only re-runs the exact selection -- the pools equal the reference's
+    per-row rebuilds."""
+    from .generation import _Pass1, _resolve_workers
+
     rows = []
+    p1, p1_error = None, None
+    try:
+        _resolve_workers(workers)
+        p1 = _Pass1(X, base_design)
+    except Exception as exc:  # every row would fail the same way
+        p1_error = exc
     for prob in probs:
         row = {"accept_prob": float(prob), "p_value": None, "n_accepted": None, "status": "ok"}
         if find_fi:
             row["fi_width"] = None
         try:
-            pool = generate_pool(X, replace(base_design, accept_prob=float(prob)), workers=workers)
+            design = replace(base_design, accept_prob=float(prob))
+            if p1_error is not None:
+                raise p1_error
+            pool = p1.pool(design)
             res = randomization_test(_observed_from_rule(obs_w_rule, pool), obs_y, pool, find_fi=find_fi,
                                      alpha=alpha)
             row["p_value"] = res.p_value

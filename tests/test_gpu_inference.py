@@ -1,6 +1,7 @@
 """GPU randomization tests and fiducial intervals vs the reference's golden
 p-values / intervals (bit-exact) and brute-force oracles."""
 
+import dataclasses
 import warnings
 
 import numpy as np
@@ -200,3 +201,21 @@ def test_c5_full_size():
     assert O.c_dim_rows(obs[None, :].astype(np.int8), y, 2500)[0] == res.tau_obs
     lo, hi = res.fi
     assert lo < res.tau_obs < hi
+
+
+def test_threshold_sweep_equals_per_probability_pools():
+    X = np.random.default_rng(31).standard_normal((40, 4))
+    y = np.random.default_rng(32).standard_normal(40)
+    for mode, extra in (("monte_carlo", dict(max_draws=20_000, batch_size=1000, root_seed=9)), ("exact", {})):
+        if mode == "exact":
+            X = np.random.default_rng(33).standard_normal((16, 3))
+            y = np.random.default_rng(34).standard_normal(16)
+        n = X.shape[0]
+        base = frr.DesignSpec(n, n // 2, accept_prob=0.5, mode=mode, **extra)
+        probs = [0.001, 0.01, 0.2, 1.0]
+        rows = frr.threshold_sweep(X, base, probs, y, find_fi=True, alpha=0.2)
+        for p, row in zip(probs, rows):
+            pool = frr.generate_pool(X, dataclasses.replace(base, accept_prob=p))
+            res = frr.randomization_test(frr.pool_assignment_matrix(pool)[0], y, pool, find_fi=True, alpha=0.2)
+            assert row["status"] == "ok" and row["p_value"] == res.p_value
+            assert row["n_accepted"] == pool.n_accepted and row["fi_width"] == res.fi[1] - res.fi[0]
