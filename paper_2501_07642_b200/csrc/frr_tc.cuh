@@ -62,7 +62,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // wait for long-idle roles: FRR_LONG_WAIT 0 = spin, 1 = hardware-suspended
 // try_wait (time hint), 2 = spin with __nanosleep backoff
 #ifndef FRR_LONG_WAIT
-#define FRR_LONG_WAIT 1
+#define FRR_LONG_WAIT 2
+#endif
+#ifndef FRR_LONG_SLEEP_NS
+#define FRR_LONG_SLEEP_NS 3000
 #endif
 __device__ __forceinline__ void mbar_wait_long(uint64_t* b, uint32_t parity) {
     const uint32_t a = smem_u32(b);
@@ -87,7 +90,7 @@ __device__ __forceinline__ void mbar_wait_long(uint64_t* b, uint32_t parity) {
 #endif
         if (ok) return;
 #if FRR_LONG_WAIT == 2
-        __nanosleep(200);
+        __nanosleep(FRR_LONG_SLEEP_NS);
 #endif
     }
 }
