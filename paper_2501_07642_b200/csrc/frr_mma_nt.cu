@@ -14,7 +14,7 @@
 // per N-chunk pass; the MMA reads A from TMEM, so only the B stream uses shared
 // memory bandwidth), then the bulk-copy warp for the int8-limb B chunks, the
 // tcgen05.mma issuer and the Fisher-Yates generator warps.
-// TMEM columns: [0, 2 NC) two accumulators, then a_st A stages of KC/4 columns.
+// TMEM columns: [0, 2 NC) two accumulators, then nst A stages of KC/4 columns.
 #include <cuda_runtime.h>
 
 #include "frr_common.cuh"
@@ -26,8 +26,8 @@ using namespace frr_tc;
 
 constexpr int BM = 128;
 constexpr int KC = 128;  // K bytes per stage
-#ifndef FRR_NT_AST
-#define FRR_NT_AST 3
+#ifndef FRR_NT_ST
+#define FRR_NT_ST 4
 #endif
 #ifndef FRR_NT_NFY
 #define FRR_NT_NFY 8
@@ -35,13 +35,17 @@ constexpr int KC = 128;  // K bytes per stage
 #ifndef FRR_NT_NEXP
 #define FRR_NT_NEXP 8
 #endif
+// timing experiments only (results invalid): 1 no B loads, 2 no A stores,
+// 4 no epilogue work, 8 no Fisher-Yates
+#ifndef FRR_NT_DEBUG
+#define FRR_NT_DEBUG 0
+#endif
 #ifndef FRR_NT_HWWAIT
 #define FRR_NT_HWWAIT 0
 #endif
-#ifndef FRR_NT_BST
-#define FRR_NT_BST 4
-#endif
-constexpr int A_ST = FRR_NT_AST, B_ST = FRR_NT_BST;  // A stages live in TMEM (max A_ST)
+// K-stage ring: stage s = A chunk s in TMEM + B chunk s in shared memory, one
+// "stage consumed" barrier (a single tcgen05.commit) releases both halves.
+constexpr int NST = FRR_NT_ST;
 constexpr int NFY = FRR_NT_NFY;
 constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
 constexpr int W_EXP0 = 4, W_TMA = W_EXP0 + NEXP, W_MMA = W_TMA + 1, W_FY0 = W_MMA + 1;
@@ -80,7 +84,7 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     size_t o = 0;
     p.a = o;
     p.b = o;
-    o += (size_t)B_ST * s.nc * KC;
+    o += (size_t)NST * s.nc * KC;
     p.bits = o;
     o += (size_t)2 * BM * (s.kw + 4) * 4;
     p.tables = o;
@@ -97,9 +101,8 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     return p;
 }
 
-constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_A_EMPTY = B_A_FULL + A_ST;
-constexpr int B_B_FULL = B_A_EMPTY + A_ST, B_B_EMPTY = B_B_FULL + B_ST;
-constexpr int B_TM_FULL = B_B_EMPTY + B_ST, B_TM_EMPTY = B_TM_FULL + 2;
+constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = B_A_FULL + NST;
+constexpr int B_S_EMPTY = B_B_FULL + NST, B_TM_FULL = B_S_EMPTY + NST, B_TM_EMPTY = B_TM_FULL + 2;
 static_assert(B_TM_EMPTY + 2 <= 30, "barrier slots");
 
 // numpy pairwise plan over d: leaves (<= 128, starting at multiples of 8),
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
     const int rowstride = S.kw + 4;
-    const int a_st = min(A_ST, (512 - 2 * S.nc) / (KC / 4));  // A stages that fit in TMEM
+    const int nst = min(NST, (512 - 2 * S.nc) / (KC / 4));  // ring stages whose A fits in TMEM
 
     for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
     __syncthreads();
@@ -188,13 +191,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_init(&bars[B_BITS_FULL + 1], NFY);
         mbar_init(&bars[B_BITS_EMPTY + 0], NEXP);
         mbar_init(&bars[B_BITS_EMPTY + 1], NEXP);
-        for (int s = 0; s < a_st; s++) {
+        for (int s = 0; s < nst; s++) {
             mbar_init(&bars[B_A_FULL + s], NEXP);
-            mbar_init(&bars[B_A_EMPTY + s], 1);
-        }
-        for (int s = 0; s < B_ST; s++) {
             mbar_init(&bars[B_B_FULL + s], 1);
-            mbar_init(&bars[B_B_EMPTY + s], 1);
+            mbar_init(&bars[B_S_EMPTY + s], 1);
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(&bars[B_TM_FULL + s], 1);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int r = fyw; r < BM; r += NFY) {
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)r * rowstride;
-                if (c < count) {
+                if (c < count && !(FRR_NT_DEBUG & 8)) {
                     frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
                     for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
                 } else {
@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int c = 0; c < S.nch; c++) {
                 for (int kc = 0; kc < S.nkc; kc++) {
                     const int s = a_s;
-                    mbar_wait_hw(&bars[B_A_EMPTY + s], a_ph ^ 1);
-                    if (++a_s == a_st) {
+                    mbar_wait_hw(&bars[B_S_EMPTY + s], a_ph ^ 1);
+                    if (++a_s == nst) {
                         a_s = 0;
                         a_ph ^= 1;
                     }
@@ -267,8 +267,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                         for (int b = 0; b < 8; b++) v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
                     }
-                    tc_st16(lane_tm + (uint32_t)(s * (KC / 4)), v);
-                    tc_wait_st();
+                    if (!(FRR_NT_DEBUG & 2)) {
+                        tc_st16(lane_tm + (uint32_t)(s * (KC / 4)), v);
+                        tc_wait_st();
+                    }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars[B_A_FULL + s]);
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_after();
                 const uint32_t cb = tl + (uint32_t)(tb * S.nc);
                 for (int g4 = 0; g4 < DJ / 8; g4++) {
+                    if (FRR_NT_DEBUG & 4) break;
                     const int j0 = c * DJ + g4 * 8;
                     if (j0 >= d) break;
                     int64_t Sj[8];
@@ -367,23 +370,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == W_TMA) {
         if (lane == 0) {
             const uint32_t bytes = (uint32_t)S.nc * KC;
-            uint32_t bstage = 0;
+            int bs = 0;
+            uint32_t bph = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int c = 0; c < S.nch; c++) {
-                    for (int kc = 0; kc < S.nkc; kc++, bstage++) {
-                        const int s = bstage % B_ST;
-                        mbar_wait_hw(&bars[B_B_EMPTY + s], ((bstage / B_ST) & 1) ^ 1);
+                    for (int kc = 0; kc < S.nkc; kc++) {
+                        const int s = bs;
+                        mbar_wait_hw(&bars[B_S_EMPTY + s], bph ^ 1);
+                        if (++bs == nst) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+#if FRR_NT_DEBUG & 1
+                        mbar_arrive(&bars[B_B_FULL + s]);  // timing experiment only: no B traffic
+#else
                         mbar_expect_tx(&bars[B_B_FULL + s], bytes);
                         bulk_g2s(sB + (size_t)s * bytes, bal.limbs + ((size_t)c * S.nkc + kc) * bytes, bytes,
                                  &bars[B_B_FULL + s]);
+#endif
                     }
                 }
             }
         }
     } else if (warp == W_MMA) {
         if (lane == 0) {
-            uint32_t chunk_ctr = 0, m_aph = 0, m_bph = 0;
-            int m_as = 0, m_bs = 0;
+            uint32_t chunk_ctr = 0, m_ph = 0;
+            int m_s = 0;
             const uint32_t b_lbo = (uint32_t)(S.nc / 8) * 128;
             const uint32_t idesc = idesc_i8(BM, S.nc);
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -393,27 +405,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     tc_fence_after();
                     const uint32_t dt = tmem_base + (uint32_t)(tb * S.nc);
                     for (int kc = 0; kc < S.nkc; kc++) {
-                        const int sa = m_as, sb = m_bs;
-                        mbar_wait(&bars[B_A_FULL + sa], m_aph);
-                        mbar_wait(&bars[B_B_FULL + sb], m_bph);
-                        if (++m_as == a_st) {
-                            m_as = 0;
-                            m_aph ^= 1;
-                        }
-                        if (++m_bs == B_ST) {
-                            m_bs = 0;
-                            m_bph ^= 1;
+                        const int st = m_s;
+                        mbar_wait(&bars[B_A_FULL + st], m_ph);
+                        mbar_wait(&bars[B_B_FULL + st], m_ph);
+                        if (++m_s == nst) {
+                            m_s = 0;
+                            m_ph ^= 1;
                         }
                         tc_fence_after();
-                        const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + sa * (KC / 4));
-                        const uint32_t b0 = smem_u32(sB + (size_t)sb * S.nc * KC);
+                        const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + st * (KC / 4));
+                        const uint32_t b0 = smem_u32(sB + (size_t)st * S.nc * KC);
 #pragma unroll
                         for (int ks = 0; ks < KC / 32; ks++) {
                             tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc,
                                          (kc | ks) != 0);
                         }
-                        tc_commit(&bars[B_A_EMPTY + sa]);
-                        tc_commit(&bars[B_B_EMPTY + sb]);
+                        tc_commit(&bars[B_S_EMPTY + st]);
                     }
                     tc_commit(&bars[B_TM_FULL + tb]);
                 }
