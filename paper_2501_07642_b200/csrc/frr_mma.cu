@@ -39,8 +39,23 @@ constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
 constexpr int A_STAGES = FRR_MMA_STAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
 constexpr int NFY = FRR_MMA_NFY;  // generator warps
-constexpr int WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
+// The warp scheduler favours higher warp ids, so the latency-critical roles
+// (tile warps, MMA issuer, bulk copies) sit above the generator warps.
+#ifndef FRR_MMA_FY_FIRST
+#define FRR_MMA_FY_FIRST 1
+#endif
+// timing experiments only (results invalid): 1 no Fisher-Yates, 4 no epilogue,
+// 8 generators only (tile, copy and MMA roles just recycle the bit buffers)
+#ifndef FRR_MMA_DEBUG
+#define FRR_MMA_DEBUG 0
+#endif
+#if FRR_MMA_FY_FIRST
+constexpr int WARP_FY0 = 0, WARP_TMA = NFY, WARP_MMA = NFY + 1, WARP_TILE0 = (NFY + 2 + 3) & ~3;
+constexpr int NWARPS = WARP_TILE0 + 4;
+#else
+constexpr int WARP_TILE0 = 0, WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
 constexpr int NWARPS = WARP_FY0 + NFY;
+#endif
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int A_STAGE_BYTES = BM * KC;
 
@@ -151,7 +166,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp >= WARP_FY0) {
+    if (warp >= WARP_FY0 && warp < WARP_FY0 + NFY) {
         // ===================================================== generators
         const int fyw = warp - WARP_FY0;
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int r = fyw; r < BM; r += NFY) {
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)r * rowstride;
-                if (c < count) {
+                if (c < count && !(FRR_MMA_DEBUG & 1)) {
                     frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
                     const int tw = frr_table_len(S.n) / 32;
                     for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
@@ -174,9 +189,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (lane == 0) mbar_arrive(&bars[BAR_BITS_FULL + buf]);
         }
-    } else if (warp < 4) {
+    } else if (warp >= WARP_TILE0 && warp < WARP_TILE0 + 4) {
         // ============================================ expansion + epilogue
-        const int r = threadIdx.x;  // tile row == TMEM lane
+        const int r = threadIdx.x - WARP_TILE0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
         const double g = bal.g, cst = bal.cst;
         const int d = S.d, full = d - (d % 8);
         int i = 0;
@@ -184,6 +199,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i & 1;
             mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i >> 1) & 1);
+            if (FRR_MMA_DEBUG & 8) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
+                continue;
+            }
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
                 const int s = astage % A_STAGES;
@@ -215,11 +235,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
             mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1);
             tc_fence_after();
-            const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
+            const uint32_t tl = tmem_base + ((uint32_t)((warp - WARP_TILE0) * 32) << 16);
             double racc[8], tq[8];
 #pragma unroll
             for (int k = 0; k < 8; k++) racc[k] = tq[k] = 0.0;
-            for (int jb = 0; jb < S.dpad; jb += 8) {
+            for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
                 int64_t Sj[8];
                 {
                     int32_t v[8];
@@ -268,7 +288,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == WARP_TMA) {
         // ============================================== B operand producer
-        if (lane == 0) {
+        if (lane == 0 && !(FRR_MMA_DEBUG & 8)) {
             const uint32_t bytes = (uint32_t)S.npad * KC;
             uint32_t bstage = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -282,7 +302,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == WARP_MMA) {
         // ===================================================== MMA issuer
-        if (lane == 0) {
+        if (lane == 0 && !(FRR_MMA_DEBUG & 8)) {
             uint32_t stage = 0;
             int i = 0;
             const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(S.npad / 8) * 128;
