@@ -130,6 +130,9 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
 #ifndef FRR_FY_ROUNDS
 #define FRR_FY_ROUNDS 2
 #endif
+#ifndef FRR_FY_REVLANE
+#define FRR_FY_REVLANE 1
+#endif
 #ifndef FRR_WALK_STREAMS
 #define FRR_WALK_STREAMS 1
 #endif
@@ -144,7 +147,12 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
     // rounds hold strictly later steps, so storing the rounds in order and
     // settling them with one verify loop keeps "last writer wins".
     uint64_t x[R];
-    x[0] = state + (uint64_t)(lane + 1) * FRR_GOLDEN;
+#if FRR_FY_REVLANE
+    const int sl = 31 - lane;  // step slot of this lane within a round
+#else
+    const int sl = lane;
+#endif
+    x[0] = state + (uint64_t)(sl + 1) * FRR_GOLDEN;
 #pragma unroll
     for (int i = 1; i < R; i++) x[i] = x[i - 1] + 32ull * FRR_GOLDEN;
     const uint64_t stride = 32ull * R * FRR_GOLDEN;
@@ -154,7 +162,7 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         uint32_t d[R], r[R], v[R], p[R];
 #pragma unroll
         for (int i = 0; i < R; i++) {
-            const int k = base + 32 * i + lane;
+            const int k = base + 32 * i + sl;
             d[i] = frr_fy_draw(x[i], steps + k, hmax);
             r[i] = (uint32_t)k + d[i];
             v[i] = (uint32_t)k + 1;
