@@ -35,7 +35,11 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_STAGES
 #define FRR_MMA_STAGES 3
 #endif
+#ifndef FRR_MMA_NBITS
+#define FRR_MMA_NBITS 3
+#endif
 constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
+constexpr int NBITS = FRR_MMA_NBITS;  // bit-row tile buffers between generators and tile warps
 constexpr int A_STAGES = FRR_MMA_STAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
 constexpr int NFY = FRR_MMA_NFY;  // generator warps
@@ -43,6 +47,25 @@ constexpr int NFY = FRR_MMA_NFY;  // generator warps
 // (tile warps, MMA issuer, bulk copies) sit above the generator warps.
 #ifndef FRR_MMA_FY_FIRST
 #define FRR_MMA_FY_FIRST 1
+#endif
+// Wait-time accounting (debug builds only): per-slot clock64 sums read back
+// with frr_debug_waits().
+#ifndef FRR_MMA_TIMING
+#define FRR_MMA_TIMING 0
+#endif
+#if FRR_MMA_TIMING
+__device__ unsigned long long g_frr_waits[16];
+#define TW(slot, ...)                          \
+    do {                                       \
+        const long long t0_ = clock64();       \
+        __VA_ARGS__;                           \
+        wacc[slot] += clock64() - t0_;         \
+    } while (0)
+#else
+#define TW(slot, ...) \
+    do {              \
+        __VA_ARGS__;  \
+    } while (0)
 #endif
 // timing experiments only (results invalid): 1 no Fisher-Yates, 4 no epilogue,
 // 8 generators only (tile, copy and MMA roles just recycle the bit buffers)
@@ -98,7 +121,7 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     p.b = o;
     o += (size_t)B_STAGES * s.npad * KC;
     p.bits = o;
-    o += (size_t)2 * BM * (s.kw + 4) * 4;
+    o += (size_t)NBITS * BM * (s.kw + 4) * 4;
     p.steps = o;
     o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
     p.tables = o;
@@ -111,8 +134,8 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
 }
 
 // barrier slots
-constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = 2;
-constexpr int BAR_A_FULL = 4, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
+constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = NBITS;
+constexpr int BAR_A_FULL = 2 * NBITS, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
 constexpr int BAR_B_FULL = BAR_A_EMPTY + A_STAGES, BAR_B_EMPTY = BAR_B_FULL + B_STAGES;
 constexpr int BAR_TMEM_FULL = BAR_B_EMPTY + B_STAGES, BAR_TMEM_EMPTY = BAR_TMEM_FULL + 1;
 constexpr int N_BARS = BAR_TMEM_EMPTY + 1;
@@ -137,13 +160,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
     const int rowstride = S.kw + 4;  // words; +16 B breaks bank aliasing of rows
+#if FRR_MMA_TIMING
+    long long wacc[16] = {0};
+    const long long tstart = clock64();
+#endif
 
     frr_fill_steps(steps, S.n, S.t);
     if (threadIdx.x == 0) {
-        mbar_init(&bars[BAR_BITS_FULL + 0], NFY);
-        mbar_init(&bars[BAR_BITS_FULL + 1], NFY);
-        mbar_init(&bars[BAR_BITS_EMPTY + 0], 4);
-        mbar_init(&bars[BAR_BITS_EMPTY + 1], 4);
+        for (int b = 0; b < NBITS; b++) {
+            mbar_init(&bars[BAR_BITS_FULL + b], NFY);
+            mbar_init(&bars[BAR_BITS_EMPTY + b], 4);
+        }
         for (int s = 0; s < A_STAGES; s++) {
             mbar_init(&bars[BAR_A_FULL + s], 4);
             mbar_init(&bars[BAR_A_EMPTY + s], 1);
@@ -172,14 +199,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i & 1;
-            mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            const int buf = i % NBITS;
+            TW(0, mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i / NBITS) & 1) ^ 1));
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
             for (int r = fyw; r < BM; r += NFY) {
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)r * rowstride;
                 if (c < count && !(FRR_MMA_DEBUG & 1)) {
-                    frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
+                    TW(11, frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane));
                     const int tw = frr_table_len(S.n) / 32;
                     for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
                 } else {
@@ -197,8 +224,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int i = 0;
         uint32_t astage = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i & 1;
-            mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i >> 1) & 1);
+            const int buf = i % NBITS;
+            TW(1, mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i / NBITS) & 1));
             if (FRR_MMA_DEBUG & 8) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
@@ -207,7 +234,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
                 const int s = astage % A_STAGES;
-                mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1);
+                TW(2, mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1));
                 const uint32_t* src = row + kc * (KC / 32);
                 uint32_t wv[KC / 32];
 #pragma unroll
@@ -233,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
 
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
-            mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1);
+            TW(3, mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1));
             tc_fence_after();
             const uint32_t tl = tmem_base + ((uint32_t)((warp - WARP_TILE0) * 32) << 16);
             double racc[8], tq[8];
@@ -294,7 +321,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kc = 0; kc < S.nkc; kc++, bstage++) {
                     const int s = bstage % B_STAGES;
-                    mbar_wait_long(&bars[BAR_B_EMPTY + s], ((bstage / B_STAGES) & 1) ^ 1);
+                    TW(4, mbar_wait_long(&bars[BAR_B_EMPTY + s], ((bstage / B_STAGES) & 1) ^ 1));
                     mbar_expect_tx(&bars[BAR_B_FULL + s], bytes);
                     bulk_g2s(sB + (size_t)s * bytes, bal.limbs + (size_t)kc * bytes, bytes, &bars[BAR_B_FULL + s]);
                 }
@@ -307,12 +334,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int i = 0;
             const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(S.npad / 8) * 128;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-                mbar_wait_long(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1);
+                TW(5, mbar_wait_long(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1));
                 tc_fence_after();
                 for (int kc = 0; kc < S.nkc; kc++, stage++) {
                     const int sa = stage % A_STAGES, sb = stage % B_STAGES;
-                    mbar_wait(&bars[BAR_A_FULL + sa], (stage / A_STAGES) & 1);
-                    mbar_wait(&bars[BAR_B_FULL + sb], (stage / B_STAGES) & 1);
+                    TW(6, mbar_wait(&bars[BAR_A_FULL + sa], (stage / A_STAGES) & 1));
+                    TW(7, mbar_wait(&bars[BAR_B_FULL + sb], (stage / B_STAGES) & 1));
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + (size_t)sa * A_STAGE_BYTES);
                     const uint32_t b0 = smem_u32(sB + (size_t)sb * S.npad * KC);
@@ -334,6 +361,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
 
+#if FRR_MMA_TIMING
+    {
+        const int role = (warp >= WARP_FY0 && warp < WARP_FY0 + NFY) ? 8 : (warp >= WARP_TILE0 && warp < WARP_TILE0 + 4) ? 9 : (warp == WARP_MMA ? 10 : 12);
+        wacc[role] += clock64() - tstart;
+        if (lane == 0)
+            for (int k = 0; k < 16; k++)
+                if (wacc[k]) atomicAdd(&g_frr_waits[k], (unsigned long long)wacc[k]);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == WARP_MMA) {
@@ -557,3 +593,13 @@ extern "C" int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int 
     k_selftest_mma<<<1, 128, smem, frr_stream(stream)>>>(A, B, K, N, D, variant);
     return frr_check_launch("k_selftest_mma");
 }
+
+#if FRR_MMA_TIMING
+extern "C" int frr_debug_waits(unsigned long long* host16) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host16, g_frr_waits, sizeof(unsigned long long) * 16);
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_frr_waits, z, sizeof(z));
+    return 0;
+}
+#endif

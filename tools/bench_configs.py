@@ -44,17 +44,29 @@ def c1():
     rng = np.random.default_rng(1)
     X = rng.standard_normal((20, 5))
     design = frr.DesignSpec(20, 10, accept_prob=0.01, mode="exact", batch_size=10_000)
+    beta, noise = rng.standard_normal(5), 0.5 * rng.standard_normal(20)
+
+    def job():
+        pool = frr.enumerate_exact(X, design)
+        obs = pool.assignments[0]
+        y = X @ beta + 1.0 * obs + noise
+        return frr.randomization_test(obs, y, pool, find_fi=True)
+
     t0 = time.perf_counter()
-    pool = frr.enumerate_exact(X, design)
-    obs = pool.assignments[0]
-    y = X @ rng.standard_normal(5) + 1.0 * obs + 0.5 * rng.standard_normal(20)
-    res = frr.randomization_test(obs, y, pool, find_fi=True)
-    wall = time.perf_counter() - t0
+    job()  # first call in the process: CUDA context, module load, allocator warm-up
+    cold = time.perf_counter() - t0
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        res = job()
+        walls.append(time.perf_counter() - t0)
+    wall = min(walls)
     kern = frr.precompute_precision(X, "exact")._kernel
     out = torch.empty(184_756, dtype=torch.float64, device="cuda")
     s = timed(lambda: G.exact_stats_device(kern, design, 0, 184_756, out))
     return {"config": "C1 exact n=20 t=10 d=5 p=0.01 + test/FI", "candidates": 184_756,
             "pass1_cand_per_s": 184_756 / s, "pass1_ms": s * 1e3, "api_wall_ms_pool_plus_test": wall * 1e3,
+            "api_wall_ms_first_call": cold * 1e3,
             "p_value": res.p_value, "fi": res.fi}
 
 
