@@ -159,7 +159,7 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
     // (padding steps k >= t have b = 1: d = 0, no store; a spurious flag from
     // them (p ~ 2^-32) only triggers the exact slow path)
     for (int base = 0; base < t; base += 32 * R) {
-        uint32_t d[R], r[R], v[R], p[R];
+        uint32_t d[R], r[R], v[R];
 #pragma unroll
         for (int i = 0; i < R; i++) {
             const int k = base + 32 * i + sl;
@@ -168,29 +168,52 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
             v[i] = (uint32_t)k + 1;
             x[i] += stride;
         }
+        // store (self-swaps change nothing), then re-read: a higher lane's
+        // store can be overwritten by a lower lane's in the same instruction,
+        // so retry until the largest k holds (values at a position only grow,
+        // so "pending" is recomputed from a fresh read each time; r = k may
+        // lie past the table when d = 0, hence the d != 0 predicate)
+#if FRR_FY_ROUNDS == 2
+        const uint32_t lwa = (uint32_t)__cvta_generic_to_shared(lw);
+        uint32_t any;
+        asm volatile(
+            "{\n\t.reg .pred q0, q1;\n\t.reg .u32 x0, x1;\n\t"
+            "setp.ne.u32 q0, %1, 0;\n\t"
+            "setp.ne.u32 q1, %4, 0;\n\t"
+            "@q0 st.shared.u16 [%2], %3;\n\t"
+            "@q1 st.shared.u16 [%5], %6;\n\t"
+            "bar.warp.sync 0xffffffff;\n\t"
+            "@q0 ld.shared.u16 x0, [%2];\n\t"
+            "@q1 ld.shared.u16 x1, [%5];\n\t"
+            "@q0 setp.lt.u32 q0, x0, %3;\n\t"
+            "@q1 setp.lt.u32 q1, x1, %6;\n\t"
+            "or.pred q0, q0, q1;\n\t"
+            "vote.sync.any.pred q0, q0, 0xffffffff;\n\t"
+            "selp.u32 %0, 1, 0, q0;\n\t}"
+            : "=r"(any)
+            : "r"(d[0]), "r"(lwa + 2u * r[0]), "r"(v[0]), "r"(d[1]), "r"(lwa + 2u * r[1]), "r"(v[1])
+            : "memory");
+        if (any) {
+#else
 #pragma unroll
         for (int i = 0; i < R; i++)
-            if (d[i] != 0) lw[r[i]] = (uint16_t)v[i];  // self-swaps change nothing
+            if (d[i] != 0) lw[r[i]] = (uint16_t)v[i];
         __syncwarp();
-        // a higher lane's store can be overwritten by a lower lane's in the
-        // same instruction: re-read and retry until the largest k holds
         bool pend = false;
 #pragma unroll
-        for (int i = 0; i < R; i++) {
-            p[i] = d[i] != 0 ? (uint32_t)lw[r[i]] < v[i] : 0u;  // r = k may lie past the table when d = 0
-            pend |= p[i] != 0;
-        }
-        while (__any_sync(FRR_FULL, pend)) {
+        for (int i = 0; i < R; i++) pend |= d[i] != 0 && (uint32_t)lw[r[i]] < v[i];
+        if (__any_sync(FRR_FULL, pend)) {
+#endif
+            bool pend;
+            do {
 #pragma unroll
-            for (int i = 0; i < R; i++)
-                if (p[i]) lw[r[i]] = (uint16_t)v[i];
-            __syncwarp();
-            pend = false;
+                for (int i = 0; i < R; i++)
+                    if (d[i] != 0 && (uint32_t)lw[r[i]] < v[i]) lw[r[i]] = (uint16_t)v[i];
+                __syncwarp();
+                pend = false;
 #pragma unroll
-            for (int i = 0; i < R; i++) {
-                if (p[i]) p[i] = (uint32_t)lw[r[i]] < v[i];
-                pend |= p[i] != 0;
-            }
+                for (int i = 0; i < R; i++) pend |= d[i] != 0 && (uint32_t)lw[r[i]] < v[i];
+            } while (__any_sync(FRR_FULL, pend));
         }
     }
     __syncwarp();
