@@ -66,6 +66,11 @@ const char* frr_last_error(void);
 int frr_device_info(int* sm_count, int* cc_major, int* cc_minor);
 
 /* ---- balance-operand preparation ------------------------------------- */
+/* Which tensor-core kernel serves (n, d, n_limbs): 0 none, 1 single-pass
+ * (N = n_limbs * d_pad <= 512 TMEM columns), 2 N-tiled.  The N-tiled kernel's
+ * B operand is pre-shifted: its limbs encode zq * 2^(3 - (k/4 mod 4)) for K
+ * offset k of each 32-unit group, so n_limbs must cover 8 * max|zq|. */
+int frr_tc_kernel(int n, int d, int n_limbs);
 /* Bytes of the tiled int8-limb B operand for (n, d, n_limbs). */
 size_t frr_limbs_bytes(int n, int d, int n_limbs);
 /* Split zq into n_limbs balanced int8 digits and tile them in the tcgen05

@@ -47,6 +47,7 @@ SIGNATURES = {
     "frr_abi_version": (i32, []),
     "frr_last_error": (ctypes.c_char_p, []),
     "frr_device_info": (i32, [ctypes.POINTER(i32)] * 3),
+    "frr_tc_kernel": (i32, [i32, i32, i32]),
     "frr_limbs_bytes": (sz, [i32, i32, i32]),
     "frr_prepare_limbs": (i32, [vp, i32, i32, i32, vp, vp, vp]),
     "frr_mc_stats": (i32, [ctypes.POINTER(Balance), u64, u64, i64, vp, vp]),

@@ -528,6 +528,8 @@ bool frr_mma_supported(const frr_balance_t* bal) {
     return tc_layout(bal->n, bal->d, bal->n_limbs) != TC_NONE;
 }
 
+extern "C" int frr_tc_kernel(int n, int d, int n_limbs) { return (int)tc_layout(n, d, n_limbs); }
+
 extern "C" size_t frr_limbs_bytes(int n, int d, int n_limbs) {
     switch (tc_layout(n, d, n_limbs)) {
         case TC_SINGLE: {

@@ -40,6 +40,13 @@ constexpr int KC = 128;  // K bytes per stage
 #ifndef FRR_NT_DEBUG
 #define FRR_NT_DEBUG 0
 #endif
+#ifndef FRR_NT_LEAN_ISSUE
+#define FRR_NT_LEAN_ISSUE 1
+#endif
+// A expansion with one LOP3 per output register (pre-shifted B operand)
+#ifndef FRR_NT_PRESHIFT
+#define FRR_NT_PRESHIFT 1
+#endif
 #ifndef FRR_NT_HWWAIT
 #define FRR_NT_HWWAIT 0
 #endif
@@ -101,7 +108,12 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     return p;
 }
 
-constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = B_A_FULL + NST;
+#ifndef FRR_NT_ONEFULL
+#define FRR_NT_ONEFULL 1
+#endif
+// FRR_NT_ONEFULL: one "stage full" barrier per ring slot, arrived on by the 8
+// expansion warps and by the bulk copy (arrive + expect_tx)
+constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = FRR_NT_ONEFULL ? B_A_FULL : B_A_FULL + NST;
 constexpr int B_S_EMPTY = B_B_FULL + NST, B_TM_FULL = B_S_EMPTY + NST, B_TM_EMPTY = B_TM_FULL + 2;
 static_assert(B_TM_EMPTY + 2 <= 30, "barrier slots");
 
@@ -192,8 +204,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_init(&bars[B_BITS_EMPTY + 0], NEXP);
         mbar_init(&bars[B_BITS_EMPTY + 1], NEXP);
         for (int s = 0; s < nst; s++) {
-            mbar_init(&bars[B_A_FULL + s], NEXP);
-            mbar_init(&bars[B_B_FULL + s], 1);
+            mbar_init(&bars[B_A_FULL + s], FRR_NT_ONEFULL ? NEXP + 1 : NEXP);
+            if (!FRR_NT_ONEFULL) mbar_init(&bars[B_B_FULL + s], 1);
             mbar_init(&bars[B_S_EMPTY + s], 1);
         }
         for (int s = 0; s < 2; s++) {
@@ -263,9 +275,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     uint32_t v[16];
 #pragma unroll
                     for (int q = 0; q < WPT; q++) {
-                        const uint32_t w = src[q];
+                        const uint32_t w = src[q], wh = w >> 4;
 #pragma unroll
-                        for (int b = 0; b < 8; b++) v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
+                        for (int b = 0; b < 8; b++) {
+#if FRR_NT_PRESHIFT
+                            // bit 8j+b of w lands in byte j of register b with weight
+                            // 2^(b&3); the B rows carry the compensating 2^(3-(b&3))
+                            v[q * 8 + b] = (b < 4 ? w : wh) & (0x01010101u << (b & 3));
+#else
+                            v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
+#endif
+                        }
                     }
                     if (!(FRR_NT_DEBUG & 2)) {
                         tc_st16(lane_tm + (uint32_t)(s * (KC / 4)), v);
@@ -322,7 +342,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int u = 0; u < 8; u++) {
                         const int j = j0 + u;
                         const double cc = j < d ? bal.cc[j] : 0.0;
-                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), cc);
+                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> (3 * FRR_NT_PRESHIFT)), g), cc);
                         q[u] = __dmul_rn(delta, delta);
                     }
                     const int G = j0 >> 3;
@@ -398,6 +418,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int m_s = 0;
             const uint32_t b_lbo = (uint32_t)(S.nc / 8) * 128;
             const uint32_t idesc = idesc_i8(BM, S.nc);
+            const uint32_t a_t0 = tmem_base + (uint32_t)(2 * S.nc);
+            const uint64_t bdesc0 = umma_desc(smem_u32(sB), b_lbo, 128);
+            const uint32_t b_stage16 = (uint32_t)(S.nc * KC) >> 4, b_ks16 = (2 * b_lbo) >> 4;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int c = 0; c < S.nch; c++, chunk_ctr++) {
                     const int tb = chunk_ctr & 1;
@@ -407,12 +430,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int kc = 0; kc < S.nkc; kc++) {
                         const int st = m_s;
                         mbar_wait(&bars[B_A_FULL + st], m_ph);
-                        mbar_wait(&bars[B_B_FULL + st], m_ph);
+                        if (!FRR_NT_ONEFULL) mbar_wait(&bars[B_B_FULL + st], m_ph);
                         if (++m_s == nst) {
                             m_s = 0;
                             m_ph ^= 1;
                         }
                         tc_fence_after();
+#if FRR_NT_LEAN_ISSUE
+                        // descriptor of stage st, K step ks = base descriptor + address offset
+                        // (start address field: bits 0-13 in 16-byte units; shared
+                        // addresses < 256 KB never carry out of it)
+                        const uint32_t at = a_t0 + (uint32_t)st * (KC / 4);
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)st * b_stage16);
+#pragma unroll
+                        for (int ks = 0; ks < KC / 32; ks++)
+                            tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), bd + (uint64_t)(ks * b_ks16), idesc, (kc | ks) != 0);
+#else
                         const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + st * (KC / 4));
                         const uint32_t b0 = smem_u32(sB + (size_t)st * S.nc * KC);
 #pragma unroll
@@ -420,6 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc,
                                          (kc | ks) != 0);
                         }
+#endif
                         tc_commit(&bars[B_S_EMPTY + st]);
                     }
                     tc_commit(&bars[B_TM_FULL + tb]);
@@ -454,7 +488,10 @@ __global__ void k_prepare_limbs_nt(const int64_t* __restrict__ zq, NtShape S, in
         const int l = nrow / DJ, j = c * DJ + nrow % DJ;
         int8_t v = 0;
         if (k < S.n && j < S.d && l < S.L) {
-            int64_t z = zq[(size_t)k * S.d + j];
+            // pre-shifted rows: K offset r of a 32-group is expanded with weight
+            // 2^((r>>2)&3), so its limbs encode z * 2^(3-((r>>2)&3)) (all
+            // products carry 8; the epilogue divides the exact sum by 8)
+            int64_t z = zq[(size_t)k * S.d + j] * (FRR_NT_PRESHIFT ? (int64_t)(8 >> ((kk >> 2) & 3)) : 1);
             for (int q = 0; q <= l; q++) {
                 v = (int8_t)(z & 0xFF);
                 z = (z - v) >> 8;
