@@ -68,6 +68,9 @@ for _ in range(R):
         e1.record(stream)
         torch.cuda.synchronize()
         times[i].append(e0.elapsed_time(e1))
+if os.environ.get("AB_VERBOSE"):
+    for p, t in zip(libs, times):
+        print(os.path.basename(p), " ".join(f"{M / x * 1e3 / 1e6:.0f}" for x in t))
 for p, t, b in zip(libs, times, bad):
     t = sorted(t)
     print(f"{os.path.basename(p):28s} mismatches={b:<8d} median={M / t[len(t) // 2] * 1e3:.3e} "
