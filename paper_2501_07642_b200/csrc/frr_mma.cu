@@ -35,6 +35,9 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_STAGES
 #define FRR_MMA_STAGES 3
 #endif
+#ifndef FRR_MMA_PAIR32
+#define FRR_MMA_PAIR32 0
+#endif
 #ifndef FRR_MMA_NBITS
 #define FRR_MMA_NBITS 3
 #endif
@@ -221,6 +224,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int r = threadIdx.x - WARP_TILE0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
         const double g = bal.g, cst = bal.cst;
         const int d = S.d, full = d - (d % 8);
+        // |acc| <= 128 n allows 32-bit limb pairs, but here (64-register
+        // budget, generator-bound kernel) the per-limb chain measured 1% faster
+        const bool pair32 = FRR_MMA_PAIR32 && (int64_t)S.n * 128 * 257 < (1ll << 31);
         int i = 0;
         uint32_t astage = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
@@ -268,20 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int k = 0; k < 8; k++) racc[k] = tq[k] = 0.0;
             for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
                 int64_t Sj[8];
-                {
-                    int32_t v[8];
-                    tc_ld8(tl + (uint32_t)((S.L - 1) * S.dpad + jb), v);
-                    tc_wait_ld();
-#pragma unroll
-                    for (int u = 0; u < 8; u++) Sj[u] = v[u];
-                }
-                for (int l = S.L - 2; l >= 0; l--) {
-                    int32_t v[8];
-                    tc_ld8(tl + (uint32_t)(l * S.dpad + jb), v);
-                    tc_wait_ld();
-#pragma unroll
-                    for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 256 + v[u];
-                }
+                tc_limbs8(tl + (uint32_t)jb, S.L, S.dpad, pair32, Sj);
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int j = jb + u;

@@ -326,44 +326,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (j0 >= d) break;
                     int64_t Sj[8];
                     const uint32_t cg = cb + (uint32_t)(g4 * 8);
-                    if (pair32) {
-                        // |acc| * 257 < 2^31: two limbs combine in 32 bits, pairs in 64
-                        int l = S.L - 1;
-                        if (S.L & 1) {
-                            int32_t v[8];
-                            tc_ld8(cg + (uint32_t)(l * DJ), v);
-                            tc_wait_ld();
-#pragma unroll
-                            for (int u = 0; u < 8; u++) Sj[u] = v[u];
-                            l--;
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < 8; u++) Sj[u] = 0;
-                        }
-                        for (; l > 0; l -= 2) {
-                            int32_t vh[8], vl[8];
-                            tc_ld8(cg + (uint32_t)(l * DJ), vh);
-                            tc_ld8(cg + (uint32_t)((l - 1) * DJ), vl);
-                            tc_wait_ld();
-#pragma unroll
-                            for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 65536 + (int64_t)(vh[u] * 256 + vl[u]);
-                        }
-                    } else {
-                        {
-                            int32_t v[8];
-                            tc_ld8(cg + (uint32_t)((S.L - 1) * DJ), v);
-                            tc_wait_ld();
-#pragma unroll
-                            for (int u = 0; u < 8; u++) Sj[u] = v[u];
-                        }
-                        for (int l = S.L - 2; l >= 0; l--) {
-                            int32_t v[8];
-                            tc_ld8(cg + (uint32_t)(l * DJ), v);
-                            tc_wait_ld();
-#pragma unroll
-                            for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 256 + v[u];
-                        }
-                    }
+                    tc_limbs8(cg, S.L, DJ, pair32, Sj);
                     double q[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {

@@ -163,6 +163,42 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;         // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
 }
 
+// Exact S_j = sum_l acc_l 256^l for 8 consecutive columns: limb l of column
+// u sits at TMEM column base + l*stride + u.  pair32: |acc| * 257 < 2^31, so
+// two limbs combine in 32 bits and only pairs need 64-bit arithmetic.
+__device__ __forceinline__ void tc_limbs8(uint32_t base, int L, int stride, bool pair32, int64_t (&Sj)[8]) {
+    int l = L - 1;
+    if (pair32 && !(L & 1)) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) Sj[u] = 0;
+    } else {
+        int32_t v[8];
+        tc_ld8(base + (uint32_t)(l * stride), v);
+        tc_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; u++) Sj[u] = v[u];
+        l--;
+    }
+    if (pair32) {
+        for (; l > 0; l -= 2) {
+            int32_t vh[8], vl[8];
+            tc_ld8(base + (uint32_t)(l * stride), vh);
+            tc_ld8(base + (uint32_t)((l - 1) * stride), vl);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 65536 + (int64_t)(vh[u] * 256 + vl[u]);
+        }
+    } else {
+        for (; l >= 0; l--) {
+            int32_t v[8];
+            tc_ld8(base + (uint32_t)(l * stride), v);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 8; u++) Sj[u] = Sj[u] * 256 + v[u];
+        }
+    }
+}
+
 // instruction descriptor: kind::i8, D=s32, A=s8, B=s8, K-major both
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
