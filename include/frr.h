@@ -171,6 +171,14 @@ int frr_tau_counts(const double* a, const double* b, int64_t m, const double* ta
 int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t* D, int variant,
                         void* stream);
 
+/* Integer-issue ceiling of the generator arithmetic: every thread of a
+ * persistent grid (SMs x 1024 threads) evaluates `per_thread` splitmix64 draws
+ * plus the exact bounded reduction (frr_mod_step) with its constants in
+ * registers -- no tables, no shared memory -- and folds them into *sink.
+ * Draws per second of this kernel is the peak the Fisher-Yates generators
+ * are compared against (bench.py "int_roofline"). */
+int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t* total_draws_host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,7 @@ SIGNATURES = {
     "frr_dim_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_tau_counts": (i32, [vp, vp, i64, vp, vp, i32, vp, vp]),
     "frr_selftest_mma_i8": (i32, [vp, vp, i32, i32, vp, i32, vp]),
+    "frr_microbench_draws": (i32, [i64, vp, vp, vp]),
 }
 
 _lock = threading.Lock()

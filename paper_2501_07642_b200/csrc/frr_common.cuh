@@ -58,7 +58,7 @@ struct __align__(16) StepC {
     uint64_t M;
 };
 
-__device__ __forceinline__ StepC frr_make_step(int n, int k) {
+__host__ __device__ __forceinline__ StepC frr_make_step(int n, int k) {
     StepC s;
     s.b = (uint32_t)(n - k);
     s.c2 = (uint32_t)((1ull << 32) % s.b);

@@ -676,3 +676,37 @@ extern "C" int frr_tau_counts(const double* a, const double* b, int64_t m, const
     k_tau_counts<<<grid, 256, 0, s>>>(a, b, m, taus, rhs, ntau, reinterpret_cast<unsigned long long*>(counts));
     return frr_check_launch("k_tau_counts");
 }
+
+// ------------------------------------------------------------ diagnostics
+namespace {
+// Generator arithmetic only: per draw one 64-bit counter step, splitmix64,
+// the rejection flag fold and the exact bounded reduction (frr_fy_draw minus
+// its step-table load), two independent chains per thread like the
+// generators' two rounds per iteration.
+__global__ void __launch_bounds__(256) k_microbench_draws(int64_t per_thread, StepC st, uint64_t* sink) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t x0 = frr_mix64(tid), x1 = x0 + 32ull * FRR_GOLDEN;
+    const uint64_t stride = 64ull * FRR_GOLDEN;
+    uint32_t hmax = 0, acc = 0;
+    for (int64_t i = 0; i < per_thread; i += 2) {
+        const uint64_t u0 = frr_mix64(x0), u1 = frr_mix64(x1);
+        hmax = max(hmax, max((uint32_t)(u0 >> 32), (uint32_t)(u1 >> 32)));
+        acc += frr_mod_step(u0, st) + frr_mod_step(u1, st);
+        x0 += stride;
+        x1 += stride;
+    }
+    if ((acc ^ hmax) == 0x9E3779B9u) atomicAdd(reinterpret_cast<unsigned long long*>(sink), 1ull);
+}
+}  // namespace
+
+extern "C" int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t* total_draws_host, void* stream) {
+    if (per_thread <= 0 || (per_thread & 1)) {
+        frr_set_error("frr_microbench_draws: per_thread must be positive and even");
+        return FRR_E_INVALID_DESIGN;
+    }
+    const int grid = frr_persistent_grid(k_microbench_draws, 256, 0, INT64_MAX);
+    const StepC st = frr_make_step(1000, 257);
+    k_microbench_draws<<<grid, 256, 0, frr_stream(stream)>>>(per_thread, st, sink);
+    if (total_draws_host) *total_draws_host = (int64_t)grid * 256 * per_thread;
+    return frr_check_launch("k_microbench_draws");
+}
