@@ -65,7 +65,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define FRR_LONG_WAIT 2
 #endif
 #ifndef FRR_LONG_SLEEP_NS
-#define FRR_LONG_SLEEP_NS 3000
+#define FRR_LONG_SLEEP_NS 500
 #endif
 __device__ __forceinline__ void mbar_wait_long(uint64_t* b, uint32_t parity) {
     const uint32_t a = smem_u32(b);
