@@ -216,3 +216,29 @@ def test_c4_full_size_properties():
                 assert int(lo) + i in acc
             elif s > pool.threshold_value:
                 assert int(lo) + i not in acc
+
+
+def test_c3_sampled_parity_around_threshold():
+    """C3 shape (n=2000, d=1024, ridge; the N-tiled tensor-core kernel) on a
+    3e5-draw prefix: the pool equals the oracle's selection over GPU stats
+    that are bit-exact on every accepted draw, the 1000 ranks either side of
+    the threshold and 1000 random draws (SURVEY 8(d) sampled parity)."""
+    X = np.random.default_rng(3).standard_normal((2000, 1024))
+    M, p = 300_000, 1e-4
+    design = frr.DesignSpec(2000, 1000, accept_prob=p, max_draws=M, batch_size=10_000, root_seed=43,
+                            precision_mode="ridge")
+    pool = frr.monte_carlo_pool(X, design)
+    kern = frr.precompute_precision(X, "ridge")._kernel
+    assert kern.tc_plan()[0] == 2  # N-tiled kernel serves this shape
+    st = G.mc_stats_device(kern, design, 0, M).cpu().numpy()
+    k = G._accepted_count(p, M)
+    order = np.argsort(st, kind="stable")
+    acc = np.sort(order[:k])
+    assert np.array_equal(pool.accepted_indices, acc) and np.array_equal(pool.stats, st[acc])
+    assert pool.threshold_value == st[order[k - 1]]
+    rng = np.random.default_rng(33)
+    idx = np.unique(np.concatenate([order[: k + 1000], rng.integers(0, M, size=1000)]))
+    bal = O.balance_setup(X, O.precision(X, "ridge"))
+    rows = O.c_batch_assign(43, idx.astype(np.uint64), 2000, 1000)
+    want = O.c_stats_rows(bal, rows, 1000)
+    assert np.array_equal(st[idx].view(np.uint64), want.view(np.uint64))
