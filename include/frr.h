@@ -146,6 +146,13 @@ size_t frr_select_workspace_bytes(int64_t m);
 int frr_select_compact(const double* stats, int64_t m, int64_t index_base,
                        const frr_select_state_t* st, const int64_t* tie_quota, int64_t* idx_out,
                        double* stat_out, int64_t* n_out, void* workspace, void* stream);
+/* Same, writing at most `cap` accepted entries (the first `cap` in index
+ * order); *n_out is the full accepted count.  With st->prefix = bits(h) and
+ * *tie_quota = INT64_MAX it is the order-preserving filter {i: stat <= h}
+ * used to narrow the select to a small candidate set. */
+int frr_select_compact_capped(const double* stats, int64_t m, int64_t index_base, const frr_select_state_t* st,
+                              const int64_t* tie_quota, int64_t cap, int64_t* idx_out, double* stat_out,
+                              int64_t* n_out, void* workspace, void* stream);
 
 /* ---- randomization test (inference.py:82-101, 129-182) ----------------- */
 /* Difference in means of y per assignment with numpy's pairwise reduction

@@ -64,6 +64,7 @@ SIGNATURES = {
     "frr_select_count": (i32, [vp, i64, vp, vp, vp]),
     "frr_select_workspace_bytes": (sz, [i64]),
     "frr_select_compact": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "frr_select_compact_capped": (i32, [vp, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp]),
     "frr_dim_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_exact": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),

@@ -18,6 +18,8 @@ accepted-key gather.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from . import _native as N
@@ -51,6 +53,8 @@ class DeviceSelectOps:
         return st[2:3]
 
     def compact(self, stats, index_base: int, st, quota, cap: int):
+        """Order-preserving compaction; at most `cap` entries are written,
+        n_out holds the full count."""
         torch = self.torch
         m = int(stats.shape[0])
         cap = max(1, min(int(cap), m))
@@ -58,9 +62,14 @@ class DeviceSelectOps:
         val = torch.empty(cap, dtype=torch.float64, device=st.device)
         n_out = torch.empty(1, dtype=torch.int64, device=st.device)
         ws = torch.empty(int(N.lib().frr_select_workspace_bytes(m)) // 8 + 1, dtype=torch.int64, device=st.device)
-        N.call("frr_select_compact", N.ptr(stats), m, int(index_base), N.ptr(st), N.ptr(quota), N.ptr(idx),
-               N.ptr(val), N.ptr(n_out), N.ptr(ws), N.stream_ptr())
+        N.call("frr_select_compact_capped", N.ptr(stats), m, int(index_base), N.ptr(st), N.ptr(quota), cap,
+               N.ptr(idx), N.ptr(val), N.ptr(n_out), N.ptr(ws), N.stream_ptr())
         return idx, val, n_out
+
+    def set_threshold(self, st, bits: int):
+        """State whose threshold is the given bit pattern (all 64 bits fixed)."""
+        st[0] = int(np.array([bits], dtype=np.uint64).view(np.int64)[0])
+        st[1] = -1
 
     def threshold(self, st) -> float:
         bits = int(st[0].item()) & ((1 << 64) - 1)
@@ -109,12 +118,74 @@ def default_comm():
     return LocalComm()
 
 
-def select_k_smallest(stats, index_base: int, k: int, ops, comm):
+SAMPLE = 1 << 20          # statistics sampled to bound the threshold from above
+PREFILTER_MIN = 1 << 22   # global candidate count from which the narrowing pays
+PREFILTER_MAX_Q = 0.05    # acceptance fractions above this select on the full data
+
+
+def _upper_bound_bits(stats, k: int, m_total: int, ops, comm):
+    """Bit pattern h of a statistic that bounds the k-th smallest from above
+    with overwhelming probability: the k_s-th smallest of a strided sample
+    (same on every rank), k_s = q s + 8 sqrt(q s) + 16 for q = k / M.  A bad
+    bound is detected by the caller (fewer than k statistics <= h) and only
+    costs a fall back to the full select."""
+    torch = N.torch_mod()
+    m = int(stats.shape[0])
+    s_r = max(1, min(m, SAMPLE // comm.world))
+    stride = max(1, m // s_r)
+    sample = stats[::stride][:s_r].contiguous()
+    if sample.shape[0] < s_r:  # m < s_r * stride cannot happen; keep shapes equal across ranks
+        sample = torch.cat([sample, sample.new_full((s_r - sample.shape[0],), float("inf"))])
+    if comm.world > 1:
+        sample = torch.cat(comm.all_gather(sample))
+    s = int(sample.shape[0])
+    qs = k / m_total * s
+    k_s = min(s, int(math.ceil(qs + 8.0 * math.sqrt(qs) + 16)))
+    st = ops.init(k_s, sample.device)
+    for p in range(8):
+        ops.pick(ops.hist(sample, st, p), st, p)
+    return int(st[0].item()) & ((1 << 64) - 1), k_s / s
+
+
+def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool = True):
     """Global k smallest of the sharded statistics.
 
     Returns (indices, values, threshold) on every rank: indices ascending
     (int64 tensor), values the matching statistics, threshold the k-th
-    smallest statistic (generation.py:159-169)."""
+    smallest statistic (generation.py:159-169).
+
+    For large inputs the select first narrows to C = {i: stat_i <= h} (one
+    ordered compaction pass; h an upper bound of the threshold from a
+    sample), then runs the radix passes and the final compaction on C: two
+    passes over the full statistics instead of ten.  Every statistic <= the
+    threshold is in C, so the result is the same as on the full data."""
+    torch = N.torch_mod()
+    m_total = int(stats.shape[0])
+    if comm.world > 1:
+        mt = torch.tensor([m_total], dtype=torch.int64, device=stats.device)
+        m_total = int(comm.all_reduce_(mt).item())
+    if prefilter and m_total >= PREFILTER_MIN and k <= PREFILTER_MAX_Q * m_total:
+        h, qh = _upper_bound_bits(stats, k, m_total, ops, comm)
+        sth = ops.init(k, stats.device)
+        ops.set_threshold(sth, h)
+        everything = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=stats.device)
+        m = int(stats.shape[0])
+        cap = int(qh * m * 1.25) + 4096
+        c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, cap)
+        n_c = int(c_n.item())
+        if n_c > c_idx.shape[0]:
+            c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, n_c)
+        tot = c_n.clone()
+        if comm.world > 1:
+            comm.all_reduce_(tot)
+        if int(tot.item()) >= k:
+            return _select_full(c_val[:n_c].contiguous(), 0, k, ops, comm, idx_map=c_idx[:n_c])
+    return _select_full(stats, index_base, k, ops, comm)
+
+
+def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
+    """The radix select proper; idx_map (narrowed input) maps local positions
+    to global indices before the gather."""
     torch = N.torch_mod()
     st = ops.init(k, stats.device)
     for p in range(8):
@@ -132,6 +203,8 @@ def select_k_smallest(stats, index_base: int, k: int, ops, comm):
         quota = torch.minimum(quota, eq[comm.rank : comm.rank + 1]).contiguous()
     idx, val, n_out = ops.compact(stats, index_base, st, quota, cap=k)
     thr = ops.threshold(st)
+    if idx_map is not None:
+        idx = idx_map[idx[: int(n_out.item())]]
     if comm.world == 1:
         n = int(n_out.item())
         return idx[:n], val[:n], thr

@@ -309,8 +309,20 @@ __device__ __forceinline__ void frr_table_bits(const uint16_t* lw, int n, int wo
 // ---------------------------------------------------- exact (combinadic)
 // generation.py:257-266: itertools.combinations order == lexicographic
 // combinadic unranking.  binom(a, b) exact in 64 bits for a <= 67.
+// Pascal's triangle for a <= 67 (every entry fits 64 bits), built at compile
+// time into constant memory.
+struct FrrBinomTable {
+    uint64_t v[68][68];
+    constexpr FrrBinomTable() : v() {
+        for (int a = 0; a < 68; a++)
+            for (int b = 0; b <= a; b++) v[a][b] = (b == 0 || b == a) ? 1ull : v[a - 1][b - 1] + v[a - 1][b];
+    }
+};
+static __constant__ FrrBinomTable c_frr_binom = FrrBinomTable();
+
 __device__ __forceinline__ uint64_t frr_binom(int a, int b) {
     if (b < 0 || b > a) return 0;
+    if (a < 68) return c_frr_binom.v[a][b];
     if (b > a - b) b = a - b;
     unsigned __int128 r = 1;
     for (int i = 1; i <= b; i++) r = r * (unsigned)(a - b + i) / (unsigned)i;
@@ -322,14 +334,11 @@ __device__ __forceinline__ uint64_t frr_binom(int a, int b) {
 __device__ inline void frr_unrank_to_table(uint64_t rank, int n, int t, uint16_t* lw) {
     int x = 0;
     for (int i = 0; i < t; i++) {
-        // C(n-x-1, t-i-1) as x advances, updated multiplicatively
-        int a = n - x - 1, b = t - i - 1;
-        unsigned __int128 c = frr_binom(a, b);
-        while (rank >= (uint64_t)c) {
-            rank -= (uint64_t)c;
-            // C(a-1, b) = C(a, b) * (a - b) / a
-            c = c * (unsigned)(a - b) / (unsigned)a;
-            a--;
+        // skip C(n-x-1, t-i-1) combinations per unit passed over
+        const int b = t - i - 1;
+        uint64_t c;
+        while (rank >= (c = frr_binom(n - x - 1, b))) {
+            rank -= c;
             x++;
         }
         lw[x] = 0;

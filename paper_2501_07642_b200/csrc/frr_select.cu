@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int64_t* ws, int64_t ntiles,
 
 __global__ void __launch_bounds__(kCThreads) k_compact(const uint64_t* __restrict__ bits, int64_t m, int64_t index_base,
                                                        const frr_select_state_t* st, const int64_t* tie_quota,
-                                                       const int64_t* ws, int64_t* idx_out, double* stat_out) {
+                                                       const int64_t* ws, int64_t cap, int64_t* idx_out,
+                                                       double* stat_out) {
     const uint64_t T = st->prefix;
     const int64_t quota = *tie_quota;
     int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;  // thread-contiguous run
@@ -204,8 +205,10 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const uint64_t* __restric
         bool less = v[j] < T, tie = v[j] == T;
         if (less || (tie && erank < quota)) {
             int64_t pos = lrank + (erank < quota ? erank : quota);
-            idx_out[pos] = index_base + base + j;
-            stat_out[pos] = __longlong_as_double((long long)v[j]);
+            if (pos < cap) {
+                idx_out[pos] = index_base + base + j;
+                stat_out[pos] = __longlong_as_double((long long)v[j]);
+            }
         }
         lrank += less;
         erank += tie;
@@ -257,6 +260,14 @@ extern "C" size_t frr_select_workspace_bytes(int64_t m) {
 extern "C" int frr_select_compact(const double* stats, int64_t m, int64_t index_base, const frr_select_state_t* st,
                                   const int64_t* tie_quota, int64_t* idx_out, double* stat_out, int64_t* n_out,
                                   void* workspace, void* stream) {
+    return frr_select_compact_capped(stats, m, index_base, st, tie_quota, INT64_MAX, idx_out, stat_out, n_out,
+                                     workspace, stream);
+}
+
+extern "C" int frr_select_compact_capped(const double* stats, int64_t m, int64_t index_base,
+                                         const frr_select_state_t* st, const int64_t* tie_quota, int64_t cap,
+                                         int64_t* idx_out, double* stat_out, int64_t* n_out, void* workspace,
+                                         void* stream) {
     cudaStream_t s = frr_stream(stream);
     int64_t ntiles = frr_cdiv(m, kTile);
     if (m <= 0) {
@@ -270,6 +281,7 @@ extern "C" int frr_select_compact(const double* stats, int64_t m, int64_t index_
     if (rc) return rc;
     k_tile_scan<<<1, 1024, 0, s>>>(ws, ntiles, tie_quota, n_out);
     if ((rc = frr_check_launch("k_tile_scan"))) return rc;
-    k_compact<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, index_base, st, tie_quota, ws, idx_out, stat_out);
+    k_compact<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, index_base, st, tie_quota, ws, cap, idx_out,
+                                                     stat_out);
     return frr_check_launch("k_compact");
 }

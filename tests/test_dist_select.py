@@ -15,6 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_2501_07642_b200 import _select as S
 from paper_2501_07642_b200._select import TorchComm, select_k_smallest
 
 
@@ -60,13 +61,21 @@ class NumpySelectOps:
         return (torch.from_numpy(idx + index_base), stats[torch.from_numpy(idx)],
                 torch.tensor([idx.shape[0]], dtype=torch.int64))
 
+    def set_threshold(self, st, bits):
+        st[0] = int(np.array([bits], dtype=np.uint64).view(np.int64)[0])
+        st[1] = -1
+
     def threshold(self, st):
         return float(np.array([int(st[0]) & (2**64 - 1)], dtype=np.uint64).view(np.float64)[0])
 
 
-def _worker(rank, world, port, stats, p, out):
+def _worker(rank, world, port, stats, p, out, narrow="off"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    if narrow != "off":  # exercise the sampled narrowing (and its fall back) at test sizes
+        S.PREFILTER_MIN, S.SAMPLE, S.PREFILTER_MAX_Q = 1, 512, 1.0
+        if narrow == "bad-bound":
+            S._upper_bound_bits = lambda *a: (0, 0.0)
     try:
         M = stats.shape[0]
         lo, hi = M * rank // world, M * (rank + 1) // world
@@ -84,14 +93,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,ties,p", [(2, True, 0.1), (2, False, 0.01), (3, True, 0.37)])
-def test_distributed_select_matches_stable_sort(world, ties, p):
+@pytest.mark.parametrize("world,ties,p,narrow", [(2, True, 0.1, "off"), (2, False, 0.01, "off"), (3, True, 0.37, "off"),
+                                                 (2, False, 0.01, "on"), (3, True, 0.05, "on"),
+                                                 (2, True, 0.02, "bad-bound")])
+def test_distributed_select_matches_stable_sort(world, ties, p, narrow):
     rng = np.random.default_rng(world * 7 + ties)
     M = 20011
     stats = np.round(rng.random(M) * (3 if ties else 1e6)) / 7.0
     with mp.Manager() as man:
         out = man.dict()
-        mp.spawn(_worker, args=(world, _free_port(), stats, p, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), stats, p, out, narrow), nprocs=world, join=True)
         results = dict(out)
     k = max(1, math.floor(p * M))
     order = np.argsort(stats, kind="stable")

@@ -95,13 +95,25 @@ def test_acceptance_count_law():
 
 
 @pytest.mark.parametrize("M,p,ties", [(1, 1.0, False), (7, 1.0, True), (1000, 0.001, True), (100_003, 0.2, True),
-                                      (3_000_017, 1e-3, False), (2_000_000, 0.5, True)])
+                                      (3_000_017, 1e-3, False), (2_000_000, 0.5, True),
+                                      # sampled narrowing (M >= 2^22): distinct values, heavy ties, q at the cut-off
+                                      (5_000_011, 1e-3, False), (6_000_000, 1e-4, True), (4_194_304, 0.05, True)])
 def test_select_vs_oracle(M, p, ties):
     rng = np.random.default_rng(M)
     st = np.round(rng.random(M) * (5 if ties else 1e12)) / 3.0
     st[: M // 10] = 0.0  # zeros (+0.0) sort first
     acc, thr = G._select(st, p)
     want, wthr = O.c_select(st, p)
+    assert np.array_equal(acc, want) and thr == wthr
+
+
+def test_narrowing_fallback_when_bound_is_low(monkeypatch):
+    from paper_2501_07642_b200 import _select as S
+    monkeypatch.setattr(S, "_upper_bound_bits", lambda *a: (0, 0.0))  # h = +0.0: far too low
+    rng = np.random.default_rng(5)
+    st = rng.random(5_000_000) + 0.5
+    acc, thr = G._select(st, 1e-3)
+    want, wthr = O.c_select(st, 1e-3)
     assert np.array_equal(acc, want) and thr == wthr
 
 

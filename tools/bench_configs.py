@@ -105,8 +105,10 @@ def c4(M=500_000_000):
     torch.cuda.synchronize()
     del out
     torch.cuda.empty_cache()
+    full = frr.DesignSpec(34, 17, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    frr.enumerate_exact(X, full)  # first call: 18.7 GB statistics allocation enters torch's cache
     t0 = time.perf_counter()
-    pool = frr.enumerate_exact(X, frr.DesignSpec(34, 17, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9))
+    pool = frr.enumerate_exact(X, full)
     wall = time.perf_counter() - t0
     return {"config": "C4 exact n=34 t=17 d=5 p=1e-3 (2.33e9 ranks)", "pass1_sample": M,
             "pass1_cand_per_s": M / s, "stat_write_GBps": gbs, "frac_hbm": gbs / PEAKS["hbm_gbs"],
