@@ -409,21 +409,55 @@ __global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t*
             pc += __popc(~word & o);
             same &= (word == o);
         }
-        // a: masked pairwise sums, one leaf per lane at a time
-        for (int L = lane; L < nleaf; L += 32) {
-            const int off = leaf_off[L], len = leaf_len[L];
-            double st = frr_pw_leaf(len, [&](int i) {
-                int e = off + i;
-                double v = __ldg(y + e);
-                return lw[e] != FRR_CTL ? v : copysign(0.0, v);
-            });
-            double sc = frr_pw_leaf(len, [&](int i) {
-                int e = off + i;
-                double v = __ldg(y + e);
-                return lw[e] != FRR_CTL ? copysign(0.0, v) : v;
-            });
-            rt[L] = st;
-            rc[L] = sc;
+        // a: masked pairwise sums.  A leaf of numpy's pairwise_sum is 8
+        // interleaved accumulator streams r_j = a[j] + a[j+8] + ... (in order)
+        // combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential
+        // tail: 8 lanes take the 8 streams of one leaf (4 leaves per warp
+        // step, coalesced y / table reads) and a butterfly forms the tree
+        // (IEEE addition is commutative, so the tree's values are exact).
+        // Masked-out terms are +-0 like the reference's 0.0*y.
+        {
+            const int g = lane >> 3, j = lane & 7;
+            for (int L0 = 0; L0 < nleaf; L0 += 4) {
+                const int L = L0 + g;
+                const bool act = L < nleaf;
+                const int off = act ? leaf_off[L] : 0, len = act ? leaf_len[L] : 0;
+                const int full = len >= 8 ? len - (len % 8) : 0;
+                double st = 0.0, sc = 0.0;
+                if (j < full) {
+                    for (int i = j; i < full; i += 8) {
+                        const int e = off + i;
+                        const double v = __ldg(y + e), z = copysign(0.0, v);
+                        const bool tr = lw[e] != FRR_CTL;
+                        const double vt = tr ? v : z, vc = tr ? z : v;
+                        if (i == j) {
+                            st = vt;
+                            sc = vc;
+                        } else {
+                            st = __dadd_rn(st, vt);
+                            sc = __dadd_rn(sc, vc);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    const double ot = __shfl_xor_sync(FRR_FULL, st, o), oc = __shfl_xor_sync(FRR_FULL, sc, o);
+                    st = __dadd_rn(st, ot);
+                    sc = __dadd_rn(sc, oc);
+                }
+                if (act && j == 0) {
+                    if (len < 8) st = sc = -0.0;
+                    for (int i = full; i < len; i++) {  // tail (or a whole short leaf)
+                        const int e = off + i;
+                        const double v = __ldg(y + e), z = copysign(0.0, v);
+                        const bool tr = lw[e] != FRR_CTL;
+                        st = __dadd_rn(st, tr ? v : z);
+                        sc = __dadd_rn(sc, tr ? z : v);
+                    }
+                    rt[L] = st;
+                    rc[L] = sc;
+                }
+            }
         }
         for (int o = 16; o > 0; o >>= 1) {
             pt += __shfl_xor_sync(FRR_FULL, pt, o);
