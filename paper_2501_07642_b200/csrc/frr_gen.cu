@@ -6,13 +6,18 @@
 // place; nothing per candidate but its statistic reaches HBM.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
 
 namespace {
 
-constexpr int kWarps = 8;  // max warps per CTA for the warp-per-candidate kernels
+constexpr int kWarps = 8;  // warps per CTA of k_exact_small
 constexpr int kThreads = kWarps * 32;
+constexpr int kPlanWarps = 16;  // max warps per CTA of the warp-per-candidate kernels
+constexpr int kPlanThreads = kPlanWarps * 32;
 
 // Shared-memory plan of a warp-per-candidate kernel: the Fisher-Yates step
 // table (shared, or global when t is too large), fixed per-CTA bytes, and a
@@ -23,19 +28,33 @@ struct WarpPlan {
     size_t smem;
 };
 
+// Picks (warps per CTA, step table placement) maximising resident warps per
+// SM: a shared step table costs every CTA its bytes, a global one (L1
+// cached) frees them for more candidate tables.
 WarpPlan plan_warps(int t, bool needs_steps, size_t fixed, size_t per_warp) {
-    const size_t cap = 227 * 1024 - 1024;
+    const size_t cap = 227 * 1024 - 1024, sm_bytes = 228 * 1024;
     const size_t steps_b = needs_steps ? (size_t)frr_steps_len(t) * sizeof(StepC) : 0;
+    WarpPlan best{0, false, 0};
+    int best_res = 0;
     for (int g = 0; g < 2; g++) {
         const bool gsteps = g == 1;
         if (gsteps && !needs_steps) break;
         const size_t f = fixed + (gsteps ? 0 : steps_b);
-        if (f + per_warp > cap) continue;
-        const int w = (int)std::min<size_t>(kWarps, (cap - f) / per_warp);
-        if (!gsteps && needs_steps && w < 4) continue;
-        return {w, gsteps, f + (size_t)w * per_warp};
+        for (int w = 1; w <= kPlanWarps; w++) {
+            const size_t smem = f + (size_t)w * per_warp;
+            if (smem > cap) break;
+            const int ctas = (int)std::min<size_t>(std::min<size_t>(sm_bytes / (smem + 1024), 64 / w), 32);
+            if (ctas < 1) continue;
+            // a shared step table saves a global (L1) load per draw: worth
+            // ~25% fewer resident warps
+            const int res = gsteps ? (ctas * w * 4) / 5 : ctas * w;
+            if (res > best_res || (res == best_res && !gsteps && best.gsteps)) {
+                best = {w, gsteps, smem};
+                best_res = res;
+            }
+        }
     }
-    return {0, false, 0};
+    return best;
 }
 
 // per-CTA steps pointer: shared copy (filled here) or the global table
@@ -83,7 +102,7 @@ __device__ __forceinline__ uint32_t table_word(const uint16_t* lw, int n, int w)
 
 // ------------------------------------------------------------- regeneration
 template <int SRC, bool GS>
-__global__ void __launch_bounds__(kThreads) k_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n,
+__global__ void __launch_bounds__(kPlanThreads) k_regen(uint64_t seed, const uint64_t* ids, int64_t m, int n,
                                                     int t, int8_t* rows, uint32_t* bits, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned char* cursor = smem;
@@ -171,7 +190,7 @@ __device__ __forceinline__ void warp_sum(int64_t (&a)[D]) {
 // S = colsum - sum over control units of Zq rows (exact int64), warp
 // reduction, then the fp64 epilogue on lane 0.
 template <int SRC, int D, bool GS>
-__global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
+__global__ void __launch_bounds__(kPlanThreads) k_stats_small(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
                                                           const int8_t* rows, uint64_t lo, int64_t count,
                                                           double* out, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_stats_small(frr_balance_t bal, uin
 // Lanes own columns j; S_j = colsum_j - sum_{control e} Zq[e][j]; q_j to a
 // per-warp scratch; lane 0 runs the exact numpy pairwise sum.
 template <int SRC, bool GS>
-__global__ void __launch_bounds__(kThreads) k_stats_generic(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
+__global__ void __launch_bounds__(kPlanThreads) k_stats_generic(frr_balance_t bal, uint64_t seed, const uint64_t* ids,
                                                             const int8_t* rows, uint64_t lo, int64_t count,
                                                             double* out, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -224,7 +243,8 @@ __global__ void __launch_bounds__(kThreads) k_stats_generic(frr_balance_t bal, u
     const StepC* steps = cta_steps<GS>(cursor, gsteps, n, t, SRC == SRC_KEYS);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     double* scratch = reinterpret_cast<double*>(cursor);
-    uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (size_t)nw * d);
+    // candidate tables start 16-byte aligned (uint4 fills) for any nw * d
+    uint16_t* tables = reinterpret_cast<uint16_t*>(scratch + (((size_t)nw * d + 1) & ~(size_t)1));
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
     double* q = scratch + (size_t)warp * d;
     __syncthreads();
@@ -367,7 +387,7 @@ __device__ void plan_build(PwPlan& P, int off, int len) {
 __host__ __device__ inline int plan_max_leaves(int n) { return n / 64 + 2; }
 
 template <int SRC, bool GS>
-__global__ void __launch_bounds__(kThreads) k_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows,
+__global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows,
                                                   int64_t m, int n, int t, const double* __restrict__ y,
                                                   const uint32_t* __restrict__ obs, double* a, double* b,
                                                   int32_t* match, const StepC* gsteps) {
@@ -554,10 +574,12 @@ int launch_planned(const char* what, KS ks, KG kg, const WarpPlan& P, int n, int
         if ((rc = gs.init(n, t, s))) return rc;
         if ((rc = frr_prepare_kernel(kg, P.smem))) return rc;
         int grid = frr_persistent_grid(kg, threads, P.smem, frr_cdiv(items, P.warps));
+        if (getenv("FRR_DEBUG_PLAN")) fprintf(stderr, "%s: warps=%d gsteps=1 smem=%zu grid=%d\n", what, P.warps, P.smem, grid);
         kg<<<grid, threads, P.smem, s>>>(args..., gs.p);
     } else {
         if ((rc = frr_prepare_kernel(ks, P.smem))) return rc;
         int grid = frr_persistent_grid(ks, threads, P.smem, frr_cdiv(items, P.warps));
+        if (getenv("FRR_DEBUG_PLAN")) fprintf(stderr, "%s: warps=%d gsteps=0 smem=%zu grid=%d\n", what, P.warps, P.smem, grid);
         ks<<<grid, threads, P.smem, s>>>(args..., (const StepC*)nullptr);
     }
     (void)keys;
@@ -592,7 +614,7 @@ int launch_stats(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, c
     if (bal->d <= 4) return launch_small<SRC, 4>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 8) return launch_small<SRC, 8>(bal, seed, ids, rows, lo, count, out, stream);
     if (bal->d <= 16) return launch_small<SRC, 16>(bal, seed, ids, rows, lo, count, out, stream);
-    WarpPlan P = plan_warps(bal->t, SRC == SRC_KEYS, 0, (size_t)bal->d * sizeof(double) + table_bytes1(bal->n));
+    WarpPlan P = plan_warps(bal->t, SRC == SRC_KEYS, 16, (size_t)bal->d * sizeof(double) + table_bytes1(bal->n));
     return launch_planned("k_stats_generic", k_stats_generic<SRC, false>, k_stats_generic<SRC, true>, P, bal->n,
                           bal->t, SRC == SRC_KEYS, count, stream, *bal, seed, ids, rows, lo, count, out);
 }
