@@ -23,7 +23,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -59,22 +58,20 @@ class ClockSampler:
         self.samples = []
         self.proc = None
 
+    # nvidia-smi writes to a temporary file that is parsed after the timed
+    # region: a reader thread in this interpreter would contend for the GIL
+    # with the step's host orchestration and show up as ~5% step time.
     def __enter__(self):
+        import tempfile
+
+        self.log = tempfile.TemporaryFile(mode="w+")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+                 "-lms", "200"], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,6 +80,12 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        self.log.seek(0)
+        for line in self.log:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+        self.log.close()
 
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
