@@ -69,7 +69,10 @@ def test_hand_value():
 MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (300, 80, 150, "exact"),
             (1000, 64, 500, "exact"), (1000, 64, 1, "exact"), (1000, 64, 999, "exact"), (2000, 70, 1000, "exact"),
             (4500, 32, 2250, "exact"), (1000, 8, 500, "exact"), (5000, 3, 2500, "exact"), (200, 130, 100, "ridge"),
-            (2000, 1024, 1000, "ridge"), (1000, 1001, 17, "ridge"), (129, 300, 64, "diagonal")]
+            (2000, 1024, 1000, "ridge"), (1000, 1001, 17, "ridge"), (129, 300, 64, "diagonal"),
+            # N-tiled kernel corner cases: odd limb count of 8*Zq (L=7), d not a
+            # multiple of 32, tiny t; n=8200 x d=96 fits neither tensor-core kernel
+            (20, 100, 10, "ridge"), (8200, 96, 4100, "exact"), (3000, 333, 2, "ridge")]
 
 
 @pytest.mark.parametrize("n,d,t,mode", MC_CASES)
@@ -81,6 +84,8 @@ def test_mc_stats_vs_oracle(n, d, t, mode, path, monkeypatch):
         M = 1024 if path == "auto" else 64
     monkeypatch.setenv("FRR_MC_PATH", path)
     kern = frr.precompute_precision(X, mode)._kernel
+    if path == "auto" and (n, d) in ((20, 100), (3000, 333), (8200, 96)):
+        assert kern.tc_plan() == {(20, 100): (2, 7), (3000, 333): (0, kern.n_limbs), (8200, 96): (0, kern.n_limbs)}[(n, d)]
     design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=10**9, batch_size=1, root_seed=n + d + t,
                             precision_mode=mode)
     lo = 10**9 - M
