@@ -71,6 +71,7 @@ SIGNATURES = {
     "frr_tau_counts": (i32, [vp, vp, i64, vp, vp, i32, vp, vp]),
     "frr_selftest_mma_i8": (i32, [vp, vp, i32, i32, vp, i32, vp]),
     "frr_microbench_draws": (i32, [i64, vp, vp, vp]),
+    "frr_microbench_mma_i8": (i32, [i32, i32, i64, vp, vp]),
 }
 
 _lock = threading.Lock()

@@ -589,6 +589,75 @@ extern "C" int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int 
     return frr_check_launch("k_selftest_mma");
 }
 
+// ---------------------------------------------------- tensor-pipe ceiling
+namespace {
+// One CTA per SM, one thread issuing back-to-back tcgen05.mma.kind::i8
+// (M = 128, N, K = 32 per instruction, 4 per 128-byte K stage) into one
+// TMEM accumulator; A from shared memory (a_tmem = 0) or TMEM (1).  The
+// operands are zero: the tensor pipe's rate does not depend on the values.
+__global__ void __launch_bounds__(128) k_microbench_mma(int N, int a_tmem, int64_t iters) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + BM * 128;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (size_t)N * 128);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    for (int o = threadIdx.x; o < (BM + N) * 128 / 16; o += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[o] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(N / 8) * 128;
+        const uint32_t idesc = idesc_i8(BM, N);
+        const uint64_t ad0 = umma_desc(smem_u32(sA), a_lbo, 128), bd0 = umma_desc(smem_u32(sB), b_lbo, 128);
+        for (int64_t it = 0; it < iters; it++) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) {
+                const uint64_t bd = bd0 + (uint64_t)((ks * 2 * b_lbo) >> 4);
+                if (a_tmem)
+                    tc_mma_i8_ts(tmem, tmem + 256 + (uint32_t)(ks * 8), bd, idesc, (it | ks) != 0);
+                else
+                    tc_mma_i8(tmem, ad0 + (uint64_t)((ks * 2 * a_lbo) >> 4), bd, idesc, (it | ks) != 0);
+            }
+        }
+        tc_commit(bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, 0);
+    tc_fence_before();
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+}  // namespace
+
+extern "C" int frr_microbench_mma_i8(int N, int a_tmem, int64_t iters, int64_t* ops_host, void* stream) {
+    if (N < 16 || N > 256 || N % 16 || iters < 1) {
+        frr_set_error("frr_microbench_mma_i8: N must be 16..256 (multiple of 16), iters >= 1");
+        return FRR_E_INVALID_DESIGN;
+    }
+    const size_t smem = 1024 + (size_t)(BM + N) * 128 + 64;
+    int rc = frr_prepare_kernel(k_microbench_mma, smem);
+    if (rc) return rc;
+    const int grid = frr_num_sms();
+    k_microbench_mma<<<grid, 128, smem, frr_stream(stream)>>>(N, a_tmem, iters);
+    if (ops_host) *ops_host = (int64_t)grid * iters * 4 * 2 * BM * N * 32;
+    return frr_check_launch("k_microbench_mma");
+}
+
 #if FRR_MMA_TIMING
 extern "C" int frr_debug_waits(unsigned long long* host16) {
     cudaDeviceSynchronize();

@@ -88,10 +88,34 @@ def c3(M=2_000_000):
                             precision_mode="ridge")
     kern = frr.precompute_precision(X, "ridge")._kernel
     out = torch.empty(M, dtype=torch.float64, device="cuda")
-    s = timed(lambda: G.mc_stats_device(kern, design, 0, M, out), reps=1)
+    s = timed(lambda: G.mc_stats_device(kern, design, 0, M, out), reps=3)
     tf = M * 2 * 2000 * 1024 / s / 1e12
+    kind, L = kern.tc_plan()
+    kpad, dpad = (2000 + 127) // 128 * 128, (1024 + 31) // 32 * 32
+    executed = M * 2 * kpad * L * dpad / s / 1e12  # int8 tensor ops actually issued
+    peak = _mma_peak(192)
     return {"config": f"C3 MC n=2000 t=1000 d=1024 ridge (sample of {M} draws)", "pass1_cand_per_s": M / s,
-            "tensor_TFLOPs_algorithmic": tf, "path": "tensor_core" if kern.wants_tensor_cores() else "cuda_core"}
+            "tensor_TFLOPs_algorithmic": tf, "int8_TOPs_executed": executed, "limbs": L,
+            "int8_peak_TOPs_measured": peak, "frac_of_measured_int8_peak": executed / peak,
+            "peak_source": "frr_microbench_mma_i8(N=192, A in TMEM): the kernel's own MMA shape, back to back",
+            "path": {1: "tcgen05 single", 2: "tcgen05 N-tiled"}.get(kind, "cuda_core")}
+
+
+def _mma_peak(n, a_tmem=1):
+    import ctypes
+
+    from paper_2501_07642_b200 import _native as N
+
+    ops = ctypes.c_int64(0)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        N.call("frr_microbench_mma_i8", n, a_tmem, 20000, ctypes.byref(ops), N.stream_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, ops.value / (e0.elapsed_time(e1) / 1e3))
+    return best / 1e12
 
 
 def c4(M=500_000_000):

@@ -1,0 +1,28 @@
+"""Measured tcgen05 kind::i8 throughput (int8 ops/s) for M=128 and several N,
+A from shared memory or TMEM: the denominator for the C3 tensor roofline."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2501_07642_b200 import _native as N  # noqa: E402
+
+res = {}
+for a_tmem in (0, 1):
+    for n in (64, 128, 192, 256):
+        ops = ctypes.c_int64(0)
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            N.call("frr_microbench_mma_i8", n, a_tmem, 20000, ctypes.byref(ops), N.stream_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, ops.value / (e0.elapsed_time(e1) / 1e3))
+        res[f"N{n}_{'tmemA' if a_tmem else 'smemA'}"] = best / 1e12
+        print(f"N={n} A={'tmem' if a_tmem else 'smem'}: {best / 1e12:.0f} TOP/s int8", flush=True)
+print(json.dumps(res))
