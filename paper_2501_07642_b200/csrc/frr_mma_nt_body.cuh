@@ -1,0 +1,516 @@
+// frr_mma_nt_body.cuh -- the N-tiled kernel, instantiated by frr_mma_nt.cu once
+// per K-stage size (FRR_NT_KC = 128 / 256) in namespace FRR_NT_NS.
+namespace FRR_NT_NS {
+using namespace frr_tc;
+
+constexpr int BM = 128;
+constexpr int KC = FRR_NT_KC;  // K bytes per stage: this instantiation's (128 or 256)
+#ifndef FRR_NT_ST
+#define FRR_NT_ST 4
+#endif
+#ifndef FRR_NT_NFY
+#define FRR_NT_NFY 8
+#endif
+#ifndef FRR_NT_NEXP
+#define FRR_NT_NEXP 8
+#endif
+// timing experiments only (results invalid): 1 no B loads, 2 no A stores,
+// 4 no epilogue work, 8 no Fisher-Yates
+#ifndef FRR_NT_DEBUG
+#define FRR_NT_DEBUG 0
+#endif
+#ifndef FRR_NT_LEAN_ISSUE
+#define FRR_NT_LEAN_ISSUE 1
+#endif
+// A expansion with one LOP3 per output register (pre-shifted B operand)
+#ifndef FRR_NT_PRESHIFT
+#define FRR_NT_PRESHIFT 1
+#endif
+#ifndef FRR_NT_HWWAIT
+#define FRR_NT_HWWAIT 0
+#endif
+// K-stage ring: stage s = A chunk s in TMEM + B chunk s in shared memory, one
+// "stage consumed" barrier (a single tcgen05.commit) releases both halves.
+constexpr int NST = KC == 256 ? 2 : FRR_NT_ST;  // TMEM holds two 64-column A stages at KC = 256
+constexpr int NFY = FRR_NT_NFY;
+constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
+constexpr int W_EXP0 = 4, W_TMA = W_EXP0 + NEXP, W_MMA = W_TMA + 1, W_FY0 = W_MMA + 1;
+constexpr int NWARPS = W_FY0 + NFY;
+constexpr int NTHREADS = NWARPS * 32;
+constexpr int DJ = 32;  // covariates per N-chunk
+constexpr int MAX_LEAVES = 1024;
+
+struct NtShape {
+    int n, t, d, L, dpad, nch, nc, kpad, nkc, kw;
+};
+
+__host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
+    NtShape s;
+    s.n = n;
+    s.t = t;
+    s.d = d;
+    s.L = L;
+    s.dpad = (d + DJ - 1) / DJ * DJ;
+    s.nch = s.dpad / DJ;
+    s.nc = DJ * L;
+    s.kpad = (n + KC - 1) / KC * KC;
+    s.nkc = s.kpad / KC;
+    s.kw = s.kpad / 32;
+    return s;
+}
+
+struct NtPlan {
+    size_t a, b, bits, tables, starts, ncomb, bars, total;
+};
+
+__host__ __device__ inline size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
+    NtPlan p;
+    size_t o = 0;
+    p.a = o;
+    p.b = o;
+    o += (size_t)NST * s.nc * KC;
+    p.bits = o;
+    o += (size_t)2 * BM * (s.kw + 4) * 4;
+    p.tables = o;
+    o += (size_t)NFY * frr_table_len(s.n) * 2;
+    o = up(o, 16);
+    p.starts = o;
+    o += up((size_t)(s.dpad / 8 + 31) / 32 * 4, 16);
+    p.ncomb = o;
+    o += MAX_LEAVES;
+    o = up(o, 16);
+    p.bars = o;
+    o += 32 * 8 + 16;
+    p.total = o + 1024;
+    return p;
+}
+
+#ifndef FRR_NT_ONEFULL
+#define FRR_NT_ONEFULL 1
+#endif
+// FRR_NT_ONEFULL: one "stage full" barrier per ring slot, arrived on by the 8
+// expansion warps and by the bulk copy (arrive + expect_tx)
+constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = FRR_NT_ONEFULL ? B_A_FULL : B_A_FULL + NST;
+constexpr int B_S_EMPTY = B_B_FULL + NST, B_TM_FULL = B_S_EMPTY + NST, B_TM_EMPTY = B_TM_FULL + 2;
+static_assert(B_TM_EMPTY + 2 <= 30, "barrier slots");
+
+// numpy pairwise plan over d: leaves (<= 128, starting at multiples of 8),
+// "group g starts a leaf" bits and, per leaf, how many combines follow it in
+// post order (numpy's recursion: n2 = n/2 rounded down to a multiple of 8).
+__device__ void nt_build(int off, int len, uint32_t* starts, uint8_t* ncomb, int& nleaf) {
+    if (len <= 128) {
+        const int g = off / 8;
+        starts[g >> 5] |= 1u << (g & 31);
+        ncomb[nleaf++] = 0;
+        return;
+    }
+    int n2 = len / 2;
+    n2 -= n2 % 8;
+    nt_build(off, n2, starts, ncomb, nleaf);
+    nt_build(off + n2, len - n2, starts, ncomb, nleaf);
+    ncomb[nleaf - 1]++;
+}
+
+__device__ __forceinline__ void tc_st_cols(uint32_t a, const uint32_t (&v)[16]) { tc_st16(a, v); }
+__device__ __forceinline__ void tc_st_cols(uint32_t a, const uint32_t (&v)[32]) { tc_st32(a, v); }
+
+// wait with a short sleep between polls, for roles whose waits are long
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(128);
+    }
+}
+
+// hardware-suspended wait (try_wait with a time hint): no issue slots spent
+__device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
+#if FRR_NT_HWWAIT
+    const uint32_t a = smem_u32(b);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "r"(100000)
+            : "memory");
+    } while (!ok);
+#else
+    mbar_wait(b, parity);
+#endif
+}
+
+__device__ __forceinline__ double comb8(const double (&r)[8]) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                     __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_mc_stats_nt(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out,
+                  const StepC* __restrict__ steps) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const NtShape S = nt_shape(bal.n, bal.t, bal.d, bal.n_limbs);
+    const NtPlan P = nt_plan(S);
+    unsigned char* sB = smem + P.b;
+    uint32_t* sBits = reinterpret_cast<uint32_t*>(smem + P.bits);
+    uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
+    uint32_t* starts = reinterpret_cast<uint32_t*>(smem + P.starts);
+    uint8_t* ncomb = smem + P.ncomb;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (count + BM - 1) / BM;
+    const int rowstride = S.kw + 4;
+    const int nst = min(NST, (512 - 2 * S.nc) / (KC / 4));  // ring stages whose A fits in TMEM
+
+    for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nleaf = 0;
+        nt_build(0, S.d, starts, ncomb, nleaf);
+        mbar_init(&bars[B_BITS_FULL + 0], NFY);
+        mbar_init(&bars[B_BITS_FULL + 1], NFY);
+        mbar_init(&bars[B_BITS_EMPTY + 0], NEXP);
+        mbar_init(&bars[B_BITS_EMPTY + 1], NEXP);
+        for (int s = 0; s < nst; s++) {
+            mbar_init(&bars[B_A_FULL + s], FRR_NT_ONEFULL ? NEXP + 1 : NEXP);
+            if (!FRR_NT_ONEFULL) mbar_init(&bars[B_B_FULL + s], 1);
+            mbar_init(&bars[B_S_EMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; s++) {
+            mbar_init(&bars[B_TM_FULL + s], 1);
+            mbar_init(&bars[B_TM_EMPTY + s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    if (warp == W_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp >= W_FY0) {
+        // ===================================================== generators
+        const int fyw = warp - W_FY0;
+        uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
+        const int tw = frr_table_len(S.n) / 32;
+        int i = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
+            const int buf = i & 1;
+            mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
+            for (int r = fyw; r < BM; r += NFY) {
+                const int64_t c = tile * BM + r;
+                uint32_t* row = tb + (size_t)r * rowstride;
+                if (c < count && !(FRR_NT_DEBUG & 8)) {
+                    frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
+                    for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
+                } else {
+                    for (int w = lane; w < S.kw; w += 32) row[w] = 0;
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mbar_arrive(&bars[B_BITS_FULL + buf]);
+        }
+    } else if (warp >= W_EXP0 && warp < W_EXP0 + NEXP) {
+        // ============================ A expansion, once per N-chunk pass
+        constexpr int TPR = NEXP / 4;             // threads per row
+        constexpr int WPT = KC / 32 / TPR;        // bit words per thread per stage
+        static_assert(WPT == 2 || WPT == 4, "tcgen05.st.x16 / x32 cover 2 / 4 bit words");
+        const int et = threadIdx.x - W_EXP0 * 32;
+        const int r = et % BM, part = et / BM;   // r / 32 == warp % 4: this warp's TMEM lanes
+        const uint32_t lane_tm =
+            tmem_base + ((uint32_t)((r >> 5) * 32) << 16) + (uint32_t)(2 * S.nc + part * WPT * 8);
+        int i = 0;
+        int a_s = 0;
+        uint32_t a_ph = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
+            const int buf = i & 1;
+            mbar_wait_hw(&bars[B_BITS_FULL + buf], (i >> 1) & 1);
+            const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
+            for (int c = 0; c < S.nch; c++) {
+                for (int kc = 0; kc < S.nkc; kc++) {
+                    const int s = a_s;
+                    mbar_wait_hw(&bars[B_S_EMPTY + s], a_ph ^ 1);
+                    if (++a_s == nst) {
+                        a_s = 0;
+                        a_ph ^= 1;
+                    }
+                    tc_fence_after();
+                    const uint32_t* src = row + kc * (KC / 32) + part * WPT;
+                    uint32_t v[WPT * 8];
+#pragma unroll
+                    for (int q = 0; q < WPT; q++) {
+                        const uint32_t w = src[q], wh = w >> 4;
+#pragma unroll
+                        for (int b = 0; b < 8; b++) {
+#if FRR_NT_PRESHIFT
+                            // bit 8j+b of w lands in byte j of register b with weight
+                            // 2^(b&3); the B rows carry the compensating 2^(3-(b&3))
+                            v[q * 8 + b] = (b < 4 ? w : wh) & (0x01010101u << (b & 3));
+#else
+                            v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
+#endif
+                        }
+                    }
+                    if (!(FRR_NT_DEBUG & 2)) {
+                        tc_st_cols(lane_tm + (uint32_t)(s * (KC / 4)), v);
+                        tc_wait_st();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars[B_A_FULL + s]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[B_BITS_EMPTY + buf]);
+        }
+    } else if (warp < 4) {
+        // ================================================ streaming epilogue
+        const int r = threadIdx.x;  // tile row == TMEM lane
+        const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
+        const double g = bal.g, cst = bal.cst;
+        const int d = S.d;
+        // per-limb accumulators are bounded by n * 2^(3*PRESHIFT) * 128
+        const bool pair32 = (int64_t)S.n * (128 << (3 * FRR_NT_PRESHIFT)) * 257 < (1ll << 31);
+        uint32_t chunk_ctr = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            double racc[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) racc[k] = 0.0;
+            double stk[16];
+            int sp = 0, leaf = -1;
+            bool done = false;
+            for (int c = 0; c < S.nch; c++, chunk_ctr++) {
+                const int tb = chunk_ctr & 1;
+                mbar_wait_lazy(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1);
+                tc_fence_after();
+                const uint32_t cb = tl + (uint32_t)(tb * S.nc);
+                for (int g4 = 0; g4 < DJ / 8; g4++) {
+                    if (FRR_NT_DEBUG & 4) break;
+                    const int j0 = c * DJ + g4 * 8;
+                    if (j0 >= d) break;
+                    int64_t Sj[8];
+                    const uint32_t cg = cb + (uint32_t)(g4 * 8);
+                    tc_limbs8(cg, S.L, DJ, pair32, Sj);
+                    double q[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int j = j0 + u;
+                        const double cc = j < d ? bal.cc[j] : 0.0;
+                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> (3 * FRR_NT_PRESHIFT)), g), cc);
+                        q[u] = __dmul_rn(delta, delta);
+                    }
+                    const int G = j0 >> 3;
+                    if ((starts[G >> 5] >> (G & 31)) & 1u) {
+                        if (leaf >= 0) {  // close the previous leaf
+                            stk[sp++] = comb8(racc);
+                            for (int m = ncomb[leaf]; m > 0; m--) {
+                                sp--;
+                                stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                            }
+                        }
+                        leaf++;
+#pragma unroll
+                        for (int u = 0; u < 8; u++) racc[u] = q[u];
+                    } else if (j0 + 8 <= d) {
+#pragma unroll
+                        for (int u = 0; u < 8; u++) racc[u] = __dadd_rn(racc[u], q[u]);
+                    } else {  // tail of the last leaf: combine, then add sequentially
+                        double res = comb8(racc);
+#pragma unroll
+                        for (int u = 0; u < 8; u++)
+                            if (j0 + u < d) res = __dadd_rn(res, q[u]);
+                        stk[sp++] = res;
+                        for (int m = ncomb[leaf]; m > 0; m--) {
+                            sp--;
+                            stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                        }
+                        done = true;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[B_TM_EMPTY + tb]);
+            }
+            if (!done) {
+                stk[sp++] = comb8(racc);
+                for (int m = ncomb[leaf]; m > 0; m--) {
+                    sp--;
+                    stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                }
+            }
+            const int64_t cidx = tile * BM + r;
+            if (cidx < count) out[cidx] = __dmul_rn(__dadd_rn(0.0, stk[0]), cst);
+        }
+    } else if (warp == W_TMA) {
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)S.nc * KC;
+            int bs = 0;
+            uint32_t bph = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int c = 0; c < S.nch; c++) {
+                    for (int kc = 0; kc < S.nkc; kc++) {
+                        const int s = bs;
+                        mbar_wait_hw(&bars[B_S_EMPTY + s], bph ^ 1);
+                        if (++bs == nst) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+#if FRR_NT_DEBUG & 1
+                        mbar_arrive(&bars[B_B_FULL + s]);  // timing experiment only: no B traffic
+#else
+                        mbar_expect_tx(&bars[B_B_FULL + s], bytes);
+                        bulk_g2s(sB + (size_t)s * bytes, bal.limbs + ((size_t)c * S.nkc + kc) * bytes, bytes,
+                                 &bars[B_B_FULL + s]);
+#endif
+                    }
+                }
+            }
+        }
+    } else if (warp == W_MMA) {
+        if (lane == 0) {
+            uint32_t chunk_ctr = 0, m_ph = 0;
+            int m_s = 0;
+            const uint32_t b_lbo = (uint32_t)(S.nc / 8) * 128;
+            const uint32_t idesc = idesc_i8(BM, S.nc);
+            const uint32_t a_t0 = tmem_base + (uint32_t)(2 * S.nc);
+            const uint64_t bdesc0 = umma_desc(smem_u32(sB), b_lbo, 128);
+            const uint32_t b_stage16 = (uint32_t)(S.nc * KC) >> 4, b_ks16 = (2 * b_lbo) >> 4;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int c = 0; c < S.nch; c++, chunk_ctr++) {
+                    const int tb = chunk_ctr & 1;
+                    mbar_wait(&bars[B_TM_EMPTY + tb], ((chunk_ctr >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t dt = tmem_base + (uint32_t)(tb * S.nc);
+                    for (int kc = 0; kc < S.nkc; kc++) {
+                        const int st = m_s;
+                        mbar_wait(&bars[B_A_FULL + st], m_ph);
+                        if (!FRR_NT_ONEFULL) mbar_wait(&bars[B_B_FULL + st], m_ph);
+                        if (++m_s == nst) {
+                            m_s = 0;
+                            m_ph ^= 1;
+                        }
+                        tc_fence_after();
+#if FRR_NT_LEAN_ISSUE
+                        // descriptor of stage st, K step ks = base descriptor + address offset
+                        // (start address field: bits 0-13 in 16-byte units; shared
+                        // addresses < 256 KB never carry out of it)
+                        const uint32_t at = a_t0 + (uint32_t)st * (KC / 4);
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)st * b_stage16);
+#pragma unroll
+                        for (int ks = 0; ks < KC / 32; ks++)
+                            tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), bd + (uint64_t)(ks * b_ks16), idesc, (kc | ks) != 0);
+#else
+                        const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + st * (KC / 4));
+                        const uint32_t b0 = smem_u32(sB + (size_t)st * S.nc * KC);
+#pragma unroll
+                        for (int ks = 0; ks < KC / 32; ks++) {
+                            tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc,
+                                         (kc | ks) != 0);
+                        }
+#endif
+                        tc_commit(&bars[B_S_EMPTY + st]);
+                    }
+                    tc_commit(&bars[B_TM_FULL + tb]);
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_MMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+// B operand: [chunk c][kc][k16][n8][8 rows][16 B]; chunk rows [limb][32 j]
+__global__ void k_prepare_limbs_nt(const int64_t* __restrict__ zq, NtShape S, int8_t* __restrict__ limbs,
+                                   int32_t* overflow) {
+    const int64_t block = (int64_t)S.nc * KC;
+    const int64_t total = (int64_t)S.nch * S.nkc * block;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t bi = o / block;
+        const int c = (int)(bi / S.nkc), kc = (int)(bi % S.nkc);
+        const int rem = (int)(o % block);
+        const int k16 = rem / (S.nc * 16);
+        const int rem2 = rem % (S.nc * 16);
+        const int nrow = (rem2 / 128) * 8 + (rem2 % 128) / 16;
+        const int kb = rem2 % 16;
+        const int kk = kc * KC + k16 * 16 + kb;
+        const int k = frr_k_unit(kk);
+        const int l = nrow / DJ, j = c * DJ + nrow % DJ;
+        int8_t v = 0;
+        if (k < S.n && j < S.d && l < S.L) {
+            // pre-shifted rows: K offset r of a 32-group is expanded with weight
+            // 2^((r>>2)&3), so its limbs encode z * 2^(3-((r>>2)&3)) (all
+            // products carry 8; the epilogue divides the exact sum by 8)
+            int64_t z = zq[(size_t)k * S.d + j] * (FRR_NT_PRESHIFT ? (int64_t)(8 >> ((kk >> 2) & 3)) : 1);
+            for (int q = 0; q <= l; q++) {
+                v = (int8_t)(z & 0xFF);
+                z = (z - v) >> 8;
+            }
+            if (l == S.L - 1 && z != 0) atomicExch(overflow, 1);
+        }
+        limbs[o] = v;
+    }
+}
+
+
+// ------------------------------------------------------------- host side
+bool fits(int n, int d, int L) {
+    if (d < 8 || L < 1 || L > 8 || n > FRR_MAX_UNITS) return false;
+    NtShape s = nt_shape(n, n - 1, d, L);
+    if (s.nc > 256 || s.dpad / 8 > 8 * MAX_LEAVES) return false;
+    if (2 * s.nc + 2 * (KC / 4) > 512) return false;  // two accumulators + >= 2 A stages in TMEM
+    return nt_plan(s).total <= 227 * 1024;
+}
+
+size_t limbs_bytes(int n, int d, int L) {
+    NtShape s = nt_shape(n, 1, d, L);
+    return (size_t)s.nch * s.nkc * s.nc * KC;
+}
+
+int prepare_limbs(const int64_t* zq, int n, int d, int L, int8_t* limbs, int32_t* overflow, cudaStream_t s) {
+    NtShape S = nt_shape(n, 1, d, L);
+    int64_t total = (int64_t)limbs_bytes(n, d, L);
+    int grid = (int)std::min<int64_t>(frr_cdiv(total, 256), (int64_t)frr_num_sms() * 16);
+    k_prepare_limbs_nt<<<grid, 256, 0, s>>>(zq, S, limbs, overflow);
+    return frr_check_launch("k_prepare_limbs_nt");
+}
+
+int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats, void* stream) {
+    if (count <= 0) return FRR_OK;
+    cudaStream_t s = frr_stream(stream);
+    NtShape S = nt_shape(bal->n, bal->t, bal->d, bal->n_limbs);
+    NtPlan P = nt_plan(S);
+    GlobalSteps gs;
+    int rc = gs.init(bal->n, bal->t, s);
+    if (rc) return rc;
+    if ((rc = frr_prepare_kernel(k_mc_stats_nt, P.total))) return rc;
+    int64_t ntiles = frr_cdiv(count, BM);
+    int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
+    k_mc_stats_nt<<<grid, NTHREADS, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
+    return frr_check_launch("k_mc_stats_nt");
+}
+
+}  // namespace FRR_NT_NS
