@@ -56,6 +56,17 @@ def test_limbs_bytes_c2():
     assert lib.frr_limbs_bytes(1000, 64, 6) == 1024 * 384
 
 
+def test_tc_kernel_choice():
+    lib = N.load_library()
+    assert lib.frr_tc_kernel(1000, 64, 6) == 1      # C2: single pass, N = 384 columns
+    assert lib.frr_tc_kernel(2000, 1024, 6) == 2    # C3: N-tiled
+    assert lib.frr_tc_kernel(20, 100, 7) == 2       # 7 limbs: N-tiled with 128-byte K stages
+    assert lib.frr_tc_kernel(34, 5, 7) == 0         # d <= 16: CUDA-core warp kernel
+    assert lib.frr_tc_kernel(8200, 96, 6) == 0      # bit rows of n=8200 do not fit shared memory
+    # the N-tiled operand: 32-covariate chunks x 2048 K bytes x 6*32 rows
+    assert lib.frr_limbs_bytes(2000, 1024, 6) == 32 * 2048 * 192
+
+
 @pytest.mark.parametrize("n,t", [(10, 0), (10, 10), (10, 11), (1, 1)])
 def test_invalid_designs(n, t):
     with pytest.raises(E.InvalidDesignError):

@@ -117,6 +117,45 @@ def test_narrowing_fallback_when_bound_is_low(monkeypatch):
     assert np.array_equal(acc, want) and thr == wthr
 
 
+def test_capped_compaction_reports_full_count():
+    """frr_select_compact_capped as the narrowing filter {stat <= h}: only the
+    first `cap` entries (index order) are written, n_out is the full count."""
+    import torch
+
+    from paper_2501_07642_b200._select import DeviceSelectOps
+
+    rng = np.random.default_rng(8)
+    st_h = np.round(rng.random(100_000) * 1000) / 7.0
+    stats = torch.from_numpy(st_h).cuda()
+    ops = DeviceSelectOps()
+    h = float(np.sort(st_h)[5000])
+    sth = ops.init(1, stats.device)
+    ops.set_threshold(sth, int(np.array([h]).view(np.uint64)[0]))
+    everything = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=stats.device)
+    want = np.flatnonzero(st_h <= h)
+    idx, val, n = ops.compact(stats, 17, sth, everything, cap=1000)
+    assert int(n.item()) == want.shape[0] and idx.shape[0] == 1000
+    assert np.array_equal(idx.cpu().numpy(), want[:1000] + 17) and np.array_equal(val.cpu().numpy(), st_h[want[:1000]])
+
+
+def test_diagnostic_microbenchmarks_run():
+    import ctypes
+
+    import torch
+
+    from paper_2501_07642_b200 import _native as N
+
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tot, ops = ctypes.c_int64(0), ctypes.c_int64(0)
+    N.call("frr_microbench_draws", 64, N.ptr(sink), ctypes.byref(tot), N.stream_ptr())
+    N.call("frr_microbench_mma_i8", 192, 1, 16, ctypes.byref(ops), N.stream_ptr())
+    torch.cuda.synchronize()
+    per_sm = 16 * 4 * 2 * 128 * 192 * 32  # iters x 4 MMAs x 2*M*N*K, one CTA per SM
+    assert tot.value > 0 and ops.value > 0 and ops.value % per_sm == 0
+    with pytest.raises(InvalidDesignError):
+        N.call("frr_microbench_draws", 3, N.ptr(sink), ctypes.byref(tot), N.stream_ptr())
+
+
 def test_c2_prefix_pool_vs_oracle():
     X = np.random.default_rng(2).standard_normal((1000, 64))
     design = frr.DesignSpec(1000, 500, accept_prob=1e-3, max_draws=200_000, batch_size=10_000, root_seed=42)
