@@ -42,15 +42,10 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #define FRR_MMA_NBITS 3
 #endif
 constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
-constexpr int NBITS = FRR_MMA_NBITS;  // bit-row tile buffers between generators and tile warps
+constexpr int NBITS = FRR_MMA_NBITS;  // max bit-row tile buffers between generators and tile warps
 constexpr int A_STAGES = FRR_MMA_STAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
-constexpr int NFY = FRR_MMA_NFY;  // generator warps
-// The warp scheduler favours higher warp ids, so the latency-critical roles
-// (tile warps, MMA issuer, bulk copies) sit above the generator warps.
-#ifndef FRR_MMA_FY_FIRST
-#define FRR_MMA_FY_FIRST 1
-#endif
+constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: their tables share smem)
 // Wait-time accounting (debug builds only): per-slot clock64 sums read back
 // with frr_debug_waits().
 #ifndef FRR_MMA_TIMING
@@ -75,20 +70,55 @@ __device__ unsigned long long g_frr_waits[16];
 #ifndef FRR_MMA_DEBUG
 #define FRR_MMA_DEBUG 0
 #endif
-#if FRR_MMA_FY_FIRST
-constexpr int WARP_FY0 = 0, WARP_TMA = NFY, WARP_MMA = NFY + 1, WARP_TILE0 = (NFY + 2 + 3) & ~3;
-constexpr int NWARPS = WARP_TILE0 + 4;
-#else
-constexpr int WARP_TILE0 = 0, WARP_TMA = 4, WARP_MMA = 5, WARP_FY0 = 6;
-constexpr int NWARPS = WARP_FY0 + NFY;
-#endif
-constexpr int NTHREADS = NWARPS * 32;
+// Warp roles (per shape, see mma_shape): generators 0..nfy-1, then the bulk
+// copy and MMA warps, then the 4 tile warps at a multiple of 4 (warp % 4 is
+// their TMEM lane quadrant).  The scheduler favours higher warp ids, so the
+// latency-critical roles sit above the generators.
+constexpr int NTHREADS = (((NFY + 2 + 3) & ~3) + 4) * 32;  // launch bound: the largest layout
 constexpr int A_STAGE_BYTES = BM * KC;
 
 struct MmaShape {
     int n, t, d, L, dpad, npad, kpad, nkc, kw;  // kw: 32-bit words per bit row
     int nparts, part_n[2], part_off[2];
+    int nfy, nbits;                              // generator warps, bit-row buffers
+    int steps_smem;                              // step table in shared (1) or global memory
+    int w_tma, w_mma, w_tile0, nwarps;           // warp roles
 };
+
+struct SmemPlan {
+    size_t steps, tables, bits, a, b, bars, total;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
+    SmemPlan p;
+    size_t o = 0;
+    p.a = o;
+    o += (size_t)A_STAGES * A_STAGE_BYTES;
+    p.b = o;
+    o += (size_t)B_STAGES * s.npad * KC;
+    p.bits = o;
+    o += (size_t)s.nbits * BM * (s.kw + 4) * 4;
+    p.steps = o;
+    if (s.steps_smem) o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
+    p.tables = o;
+    o += (size_t)s.nfy * frr_table_len(s.n) * 2;
+    o = align_up(o, 16);
+    p.bars = o;
+    o += 32 * 8 + 16;
+    p.total = o + 1024;  // slack for base alignment
+    return p;
+}
+
+__host__ __device__ inline void set_roles(MmaShape& s, int nfy, int nbits) {
+    s.nfy = nfy;
+    s.nbits = nbits;
+    s.w_tma = nfy;
+    s.w_mma = nfy + 1;
+    s.w_tile0 = (nfy + 2 + 3) & ~3;
+    s.nwarps = s.w_tile0 + 4;
+}
 
 __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
     MmaShape s;
@@ -107,33 +137,22 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
     s.part_n[1] = s.npad - s.part_n[0];
     s.part_off[0] = 0;
     s.part_off[1] = s.part_n[0];
+    // Largest generator count with at least two bit buffers that fits shared
+    // memory (tables are 2n bytes per generator, bit buffers n/8 per row);
+    // large n falls back to one buffer and as few as 4 generators.
+    // The step table (16 B per step) moves to global memory (L1-cached) when
+    // keeping it would cost generators or buffers.
+    for (int ss = 1; ss >= 0; ss--) {
+        s.steps_smem = ss;
+        for (int nb = NBITS; nb >= 1; nb--) {
+            for (int f = NFY; f >= (nb >= 2 ? 8 : 4); f--) {
+                set_roles(s, f, nb);
+                if (smem_plan(s).total <= 227 * 1024 && (ss == 0 || (f == NFY && nb == NBITS))) return s;
+            }
+        }
+    }
+    set_roles(s, 0, 0);  // does not fit: tc_layout rejects the shape
     return s;
-}
-
-struct SmemPlan {
-    size_t steps, tables, bits, a, b, bars, total;
-};
-
-__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-__host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
-    SmemPlan p;
-    size_t o = 0;
-    p.a = o;
-    o += (size_t)A_STAGES * A_STAGE_BYTES;
-    p.b = o;
-    o += (size_t)B_STAGES * s.npad * KC;
-    p.bits = o;
-    o += (size_t)NBITS * BM * (s.kw + 4) * 4;
-    p.steps = o;
-    o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
-    p.tables = o;
-    o += (size_t)NFY * frr_table_len(s.n) * 2;
-    o = align_up(o, 16);
-    p.bars = o;
-    o += 32 * 8 + 16;
-    p.total = o + 1024;  // slack for base alignment
-    return p;
 }
 
 // barrier slots
@@ -144,18 +163,27 @@ constexpr int BAR_TMEM_FULL = BAR_B_EMPTY + B_STAGES, BAR_TMEM_EMPTY = BAR_TMEM_
 constexpr int N_BARS = BAR_TMEM_EMPTY + 1;
 static_assert(N_BARS <= 30, "barrier slots");
 
+// GS: step table in global memory (large n), else in shared memory
+// GS: step table in global memory (large n), else in shared memory.
+// FULL: NFY generator warps and NBITS bit buffers (compile-time constants).
+template <bool GS, bool FULL>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_mc_stats_mma(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out) {
+    k_mc_stats_mma(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out,
+                   const StepC* __restrict__ gsteps) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // keep the shared address space visible to the compiler (LDS/STS, not
     // generic LD/ST): align by offsetting the __shared__ array itself
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const MmaShape S = mma_shape(bal.n, bal.t, bal.d, bal.n_limbs);
     const SmemPlan P = smem_plan(S);
+    // FULL: the default layout (NFY generators, NBITS buffers) as compile-time
+    // constants -- the fast path; otherwise the shape's reduced layout
+    const int c_nfy = FULL ? NFY : S.nfy, c_nbits = FULL ? NBITS : S.nbits;
+    const int c_w_tma = c_nfy, c_w_mma = c_nfy + 1, c_w_tile0 = (c_nfy + 2 + 3) & ~3;
     unsigned char* sA = smem + P.a;
     unsigned char* sB = smem + P.b;
     uint32_t* sBits = reinterpret_cast<uint32_t*>(smem + P.bits);
-    StepC* steps = reinterpret_cast<StepC*>(smem + P.steps);
+    StepC* ssteps = reinterpret_cast<StepC*>(smem + P.steps);
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
@@ -168,10 +196,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const long long tstart = clock64();
 #endif
 
-    frr_fill_steps(steps, S.n, S.t);
+    if (!GS) frr_fill_steps(ssteps, S.n, S.t);
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBITS; b++) {
-            mbar_init(&bars[BAR_BITS_FULL + b], NFY);
+        for (int b = 0; b < c_nbits; b++) {
+            mbar_init(&bars[BAR_BITS_FULL + b], c_nfy);
             mbar_init(&bars[BAR_BITS_EMPTY + b], 4);
         }
         for (int s = 0; s < A_STAGES; s++) {
@@ -187,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
-    if (warp == WARP_MMA) {
+    if (warp == c_w_mma) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -196,20 +224,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp >= WARP_FY0 && warp < WARP_FY0 + NFY) {
+    if (warp < c_nfy) {
         // ===================================================== generators
-        const int fyw = warp - WARP_FY0;
+        const int fyw = warp;
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i % NBITS;
-            TW(0, mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i / NBITS) & 1) ^ 1));
+            const int buf = i % c_nbits;
+            TW(0, mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1));
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
-            for (int r = fyw; r < BM; r += NFY) {
+            for (int r = fyw; r < BM; r += c_nfy) {
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)r * rowstride;
                 if (c < count && !(FRR_MMA_DEBUG & 1)) {
-                    TW(11, frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane));
+                    TW(11, frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, GS ? gsteps : ssteps,
+                                       lw, lane));
                     const int tw = frr_table_len(S.n) / 32;
                     for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
                 } else {
@@ -219,9 +248,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (lane == 0) mbar_arrive(&bars[BAR_BITS_FULL + buf]);
         }
-    } else if (warp >= WARP_TILE0 && warp < WARP_TILE0 + 4) {
+    } else if (warp >= c_w_tile0 && warp < c_w_tile0 + 4) {
         // ============================================ expansion + epilogue
-        const int r = threadIdx.x - WARP_TILE0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
+        const int r = threadIdx.x - c_w_tile0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
         const double g = bal.g, cst = bal.cst;
         const int d = S.d, full = d - (d % 8);
         // |acc| <= 128 n allows 32-bit limb pairs, but here (64-register
@@ -230,8 +259,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int i = 0;
         uint32_t astage = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i % NBITS;
-            TW(1, mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i / NBITS) & 1));
+            const int buf = i % c_nbits;
+            TW(1, mbar_wait_long(&bars[BAR_BITS_FULL + buf], (i / c_nbits) & 1));
             if (FRR_MMA_DEBUG & 8) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
@@ -268,7 +297,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
             TW(3, mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1));
             tc_fence_after();
-            const uint32_t tl = tmem_base + ((uint32_t)((warp - WARP_TILE0) * 32) << 16);
+            const uint32_t tl = tmem_base + ((uint32_t)((warp - c_w_tile0) * 32) << 16);
             double racc[8], tq[8];
 #pragma unroll
             for (int k = 0; k < 8; k++) racc[k] = tq[k] = 0.0;
@@ -306,7 +335,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int64_t c = tile * BM + r;
             if (c < count) out[c] = __dmul_rn(__dadd_rn(0.0, res), cst);
         }
-    } else if (warp == WARP_TMA) {
+    } else if (warp == c_w_tma) {
         // ============================================== B operand producer
         if (lane == 0 && !(FRR_MMA_DEBUG & 8)) {
             const uint32_t bytes = (uint32_t)S.npad * KC;
@@ -320,7 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp == WARP_MMA) {
+    } else if (warp == c_w_mma) {
         // ===================================================== MMA issuer
         if (lane == 0 && !(FRR_MMA_DEBUG & 8)) {
             uint32_t stage = 0;
@@ -356,7 +385,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 #if FRR_MMA_TIMING
     {
-        const int role = (warp >= WARP_FY0 && warp < WARP_FY0 + NFY) ? 8 : (warp >= WARP_TILE0 && warp < WARP_TILE0 + 4) ? 9 : (warp == WARP_MMA ? 10 : 12);
+        const int role = warp < c_nfy ? 8 : (warp >= c_w_tile0 && warp < c_w_tile0 + 4) ? 9 : (warp == c_w_mma ? 10 : 12);
         wacc[role] += clock64() - tstart;
         if (lane == 0)
             for (int k = 0; k < 16; k++)
@@ -365,7 +394,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
     tc_fence_before();
     __syncthreads();
-    if (warp == WARP_MMA) {
+    if (warp == c_w_mma) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
@@ -509,7 +538,7 @@ enum TcLayout { TC_NONE = 0, TC_SINGLE = 1, TC_NT = 2 };
 TcLayout tc_layout(int n, int d, int L) {
     if (d <= 16 || L < 1 || L > 8 || n < 2 || n > FRR_MAX_UNITS) return TC_NONE;
     MmaShape s = mma_shape(n, n - 1, d, L);
-    if (s.npad <= 512 && smem_plan(s).total <= 227 * 1024) return TC_SINGLE;
+    if (s.npad <= 512 && s.nfy > 0) return TC_SINGLE;
     if (frr_nt_fits(n, d, L)) return TC_NT;
     return TC_NONE;
 }
@@ -559,11 +588,16 @@ int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64
     if (tc_layout(bal->n, bal->d, bal->n_limbs) == TC_NT) return frr_mc_stats_nt(bal, seed, lo, count, stats, stream);
     MmaShape S = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
     SmemPlan P = smem_plan(S);
-    int rc = frr_prepare_kernel(k_mc_stats_mma, P.total);
+    const bool full = S.nfy == NFY && S.nbits == NBITS;
+    const auto kern = S.steps_smem ? (full ? k_mc_stats_mma<false, true> : k_mc_stats_mma<false, false>)
+                                   : (full ? k_mc_stats_mma<true, true> : k_mc_stats_mma<true, false>);
+    int rc = frr_prepare_kernel(kern, P.total);
     if (rc) return rc;
     int64_t ntiles = frr_cdiv(count, BM);
     int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
-    k_mc_stats_mma<<<grid, NTHREADS, P.total, frr_stream(stream)>>>(*bal, seed, lo, count, stats);
+    GlobalSteps gs;
+    if (!S.steps_smem && (rc = gs.init(bal->n, bal->t, frr_stream(stream)))) return rc;
+    kern<<<grid, S.nwarps * 32, P.total, frr_stream(stream)>>>(*bal, seed, lo, count, stats, gs.p);
     return frr_check_launch("k_mc_stats_mma");
 }
 
