@@ -42,22 +42,8 @@ constexpr int MAX_LEAVES = 1024;
 
 struct NtShape {
     int n, t, d, L, dpad, nch, nc, kpad, nkc, kw;
+    int nfy, nbits;  // generator warps, bit-row buffers (fewer for large n)
 };
-
-__host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
-    NtShape s;
-    s.n = n;
-    s.t = t;
-    s.d = d;
-    s.L = L;
-    s.dpad = (d + DJ - 1) / DJ * DJ;
-    s.nch = s.dpad / DJ;
-    s.nc = DJ * L;
-    s.kpad = (n + KC - 1) / KC * KC;
-    s.nkc = s.kpad / KC;
-    s.kw = s.kpad / 32;
-    return s;
-}
 
 struct NtPlan {
     size_t a, b, bits, tables, starts, ncomb, bars, total;
@@ -72,9 +58,9 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     p.b = o;
     o += (size_t)NST * s.nc * KC;
     p.bits = o;
-    o += (size_t)2 * BM * (s.kw + 4) * 4;
+    o += (size_t)s.nbits * BM * (s.kw + 4) * 4;
     p.tables = o;
-    o += (size_t)NFY * frr_table_len(s.n) * 2;
+    o += (size_t)s.nfy * frr_table_len(s.n) * 2;
     o = up(o, 16);
     p.starts = o;
     o += up((size_t)(s.dpad / 8 + 31) / 32 * 4, 16);
@@ -85,6 +71,30 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     o += 32 * 8 + 16;
     p.total = o + 1024;
     return p;
+}
+
+__host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
+    NtShape s;
+    s.n = n;
+    s.t = t;
+    s.d = d;
+    s.L = L;
+    s.dpad = (d + DJ - 1) / DJ * DJ;
+    s.nch = s.dpad / DJ;
+    s.nc = DJ * L;
+    s.kpad = (n + KC - 1) / KC * KC;
+    s.nkc = s.kpad / KC;
+    s.kw = s.kpad / 32;
+    // the full layout (NFY generators, two bit buffers) when it fits, else
+    // fewer generators / one buffer so that large n keeps the tensor cores
+    for (int nb = 2; nb >= 1; nb--)
+        for (int f = NFY; f >= 2; f--) {
+            s.nfy = f;
+            s.nbits = nb;
+            if (nt_plan(s).total <= 227 * 1024) return s;
+        }
+    s.nfy = s.nbits = 0;
+    return s;
 }
 
 #ifndef FRR_NT_ONEFULL
@@ -157,6 +167,8 @@ __device__ __forceinline__ double comb8(const double (&r)[8]) {
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 }
 
+// FULL: NFY generator warps and two bit buffers as compile-time constants
+template <bool FULL>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_mc_stats_nt(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out,
                   const StepC* __restrict__ steps) {
@@ -175,16 +187,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int64_t ntiles = (count + BM - 1) / BM;
     const int rowstride = S.kw + 4;
     const int nst = min(NST, (512 - 2 * S.nc) / (KC / 4));  // ring stages whose A fits in TMEM
+    const int c_nfy = FULL ? NFY : S.nfy, c_nbits = FULL ? 2 : S.nbits;
 
     for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
         int nleaf = 0;
         nt_build(0, S.d, starts, ncomb, nleaf);
-        mbar_init(&bars[B_BITS_FULL + 0], NFY);
-        mbar_init(&bars[B_BITS_FULL + 1], NFY);
-        mbar_init(&bars[B_BITS_EMPTY + 0], NEXP);
-        mbar_init(&bars[B_BITS_EMPTY + 1], NEXP);
+        for (int b = 0; b < c_nbits; b++) {
+            mbar_init(&bars[B_BITS_FULL + b], c_nfy);
+            mbar_init(&bars[B_BITS_EMPTY + b], NEXP);
+        }
         for (int s = 0; s < nst; s++) {
             mbar_init(&bars[B_A_FULL + s], FRR_NT_ONEFULL ? NEXP + 1 : NEXP);
             if (!FRR_NT_ONEFULL) mbar_init(&bars[B_B_FULL + s], 1);
@@ -213,10 +226,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int tw = frr_table_len(S.n) / 32;
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i & 1;
-            mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i >> 1) & 1) ^ 1);
+            const int buf = i % c_nbits;
+            mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1);
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
-            for (int r = fyw; r < BM; r += NFY) {
+            for (int r = fyw; r < BM; r += c_nfy) {
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)r * rowstride;
                 if (c < count && !(FRR_NT_DEBUG & 8)) {
@@ -242,8 +255,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int a_s = 0;
         uint32_t a_ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
-            const int buf = i & 1;
-            mbar_wait_hw(&bars[B_BITS_FULL + buf], (i >> 1) & 1);
+            const int buf = i % c_nbits;
+            mbar_wait_hw(&bars[B_BITS_FULL + buf], (i / c_nbits) & 1);
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int c = 0; c < S.nch; c++) {
                 for (int kc = 0; kc < S.nkc; kc++) {
@@ -482,7 +495,7 @@ bool fits(int n, int d, int L) {
     NtShape s = nt_shape(n, n - 1, d, L);
     if (s.nc > 256 || s.dpad / 8 > 8 * MAX_LEAVES) return false;
     if (2 * s.nc + 2 * (KC / 4) > 512) return false;  // two accumulators + >= 2 A stages in TMEM
-    return nt_plan(s).total <= 227 * 1024;
+    return s.nfy > 0;
 }
 
 size_t limbs_bytes(int n, int d, int L) {
@@ -506,10 +519,12 @@ int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count
     GlobalSteps gs;
     int rc = gs.init(bal->n, bal->t, s);
     if (rc) return rc;
-    if ((rc = frr_prepare_kernel(k_mc_stats_nt, P.total))) return rc;
+    const bool full = S.nfy == NFY && S.nbits == 2;
+    const auto kern = full ? k_mc_stats_nt<true> : k_mc_stats_nt<false>;
+    if ((rc = frr_prepare_kernel(kern, P.total))) return rc;
     int64_t ntiles = frr_cdiv(count, BM);
     int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
-    k_mc_stats_nt<<<grid, NTHREADS, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
+    kern<<<grid, (W_FY0 + S.nfy) * 32, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
     return frr_check_launch("k_mc_stats_nt");
 }
 

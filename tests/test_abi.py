@@ -63,6 +63,7 @@ def test_tc_kernel_choice():
     assert lib.frr_tc_kernel(20, 100, 7) == 2       # 7 limbs: N-tiled with 128-byte K stages
     assert lib.frr_tc_kernel(34, 5, 7) == 0         # d <= 16: CUDA-core warp kernel
     assert lib.frr_tc_kernel(8200, 96, 6) == 0      # bit rows of n=8200 do not fit shared memory
+    assert lib.frr_tc_kernel(5000, 128, 6) == 2     # large n: N-tiled with one bit buffer
     # the N-tiled operand: 32-covariate chunks x 2048 K bytes x 6*32 rows
     assert lib.frr_limbs_bytes(2000, 1024, 6) == 32 * 2048 * 192
 

@@ -74,7 +74,9 @@ MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (
             # multiple of 32, tiny t; n=8200 x d=96 fits neither tensor-core kernel
             (20, 100, 10, "ridge"), (8200, 96, 4100, "exact"), (3000, 333, 2, "ridge"),
             # single-pass kernel at large n: fewer generator warps / one bit buffer
-            (5000, 64, 2500, "exact"), (3000, 40, 1500, "exact"), (12000, 24, 6000, "exact")]
+            (5000, 64, 2500, "exact"), (3000, 40, 1500, "exact"), (12000, 24, 6000, "exact"),
+            # N-tiled kernel at large n: one bit buffer, fewer generators
+            (5000, 128, 2500, "exact")]
 
 
 @pytest.mark.parametrize("n,d,t,mode", MC_CASES)
@@ -86,10 +88,11 @@ def test_mc_stats_vs_oracle(n, d, t, mode, path, monkeypatch):
         M = 1024 if path == "auto" else 64
     monkeypatch.setenv("FRR_MC_PATH", path)
     kern = frr.precompute_precision(X, mode)._kernel
-    if path == "auto" and (n, d) in ((20, 100), (3000, 333), (8200, 96), (5000, 64), (3000, 40)):
-        want = {(20, 100): (2, 7), (3000, 333): (0, kern.n_limbs), (8200, 96): (0, kern.n_limbs),
-                (5000, 64): (1, kern.n_limbs), (3000, 40): (1, kern.n_limbs)}[(n, d)]
-        assert kern.tc_plan() == want
+    if path == "auto" and (n, d) in ((20, 100), (3000, 333), (8200, 96), (5000, 64), (3000, 40), (5000, 128)):
+        want = {(20, 100): 2, (3000, 333): 2, (8200, 96): 0, (5000, 64): 1, (3000, 40): 1, (5000, 128): 2}[(n, d)]
+        assert kern.tc_plan()[0] == want
+        if (n, d) == (20, 100):
+            assert kern.tc_plan()[1] == 7  # 8*Zq needs 7 limbs: 128-byte K stages
     design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=10**9, batch_size=1, root_seed=n + d + t,
                             precision_mode=mode)
     lo = 10**9 - M
