@@ -12,9 +12,6 @@
 #define FRR_GOLDEN 0x9E3779B97F4A7C15ull
 #define FRR_FULL 0xffffffffu
 #define FRR_CTL 0xFFFFu  // table marker: unit is a control unit
-#ifndef FRR_FY_MATCH
-#define FRR_FY_MATCH 0
-#endif
 
 // ---------------------------------------------------------------- error state
 void frr_set_error(const char* fmt, ...);
@@ -130,12 +127,6 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
 #ifndef FRR_FY_ROUNDS
 #define FRR_FY_ROUNDS 2
 #endif
-#ifndef FRR_FY_REVLANE
-#define FRR_FY_REVLANE 1
-#endif
-#ifndef FRR_WALK_STREAMS
-#define FRR_WALK_STREAMS 1
-#endif
 
 __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
                                             uint16_t* lw, int lane) {
@@ -147,11 +138,11 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
     // rounds hold strictly later steps, so storing the rounds in order and
     // settling them with one verify loop keeps "last writer wins".
     uint64_t x[R];
-#if FRR_FY_REVLANE
-    const int sl = 31 - lane;  // step slot of this lane within a round
-#else
-    const int sl = lane;
-#endif
+    // step slot of this lane within a round: the highest step in the lowest
+    // lane, because same-address stores of one instruction mostly resolve in
+    // favour of the lowest lane (fewer verify retries; correctness does not
+    // depend on it)
+    const int sl = 31 - lane;
     x[0] = state + (uint64_t)(sl + 1) * FRR_GOLDEN;
 #pragma unroll
     for (int i = 1; i < R; i++) x[i] = x[i - 1] + 32ull * FRR_GOLDEN;

@@ -35,9 +35,6 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #ifndef FRR_MMA_STAGES
 #define FRR_MMA_STAGES 3
 #endif
-#ifndef FRR_MMA_PAIR32
-#define FRR_MMA_PAIR32 0
-#endif
 #ifndef FRR_MMA_NBITS
 #define FRR_MMA_NBITS 3
 #endif
@@ -253,9 +250,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int r = threadIdx.x - c_w_tile0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
         const double g = bal.g, cst = bal.cst;
         const int d = S.d, full = d - (d % 8);
-        // |acc| <= 128 n allows 32-bit limb pairs, but here (64-register
+        // |acc| <= 128 n would allow 32-bit limb pairs, but here (64-register
         // budget, generator-bound kernel) the per-limb chain measured 1% faster
-        const bool pair32 = FRR_MMA_PAIR32 && (int64_t)S.n * 128 * 257 < (1ll << 31);
+        const bool pair32 = false;
         int i = 0;
         uint32_t astage = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {

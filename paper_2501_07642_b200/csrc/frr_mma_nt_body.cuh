@@ -19,16 +19,6 @@ constexpr int KC = FRR_NT_KC;  // K bytes per stage: this instantiation's (128 o
 #ifndef FRR_NT_DEBUG
 #define FRR_NT_DEBUG 0
 #endif
-#ifndef FRR_NT_LEAN_ISSUE
-#define FRR_NT_LEAN_ISSUE 1
-#endif
-// A expansion with one LOP3 per output register (pre-shifted B operand)
-#ifndef FRR_NT_PRESHIFT
-#define FRR_NT_PRESHIFT 1
-#endif
-#ifndef FRR_NT_HWWAIT
-#define FRR_NT_HWWAIT 0
-#endif
 // K-stage ring: stage s = A chunk s in TMEM + B chunk s in shared memory, one
 // "stage consumed" barrier (a single tcgen05.commit) releases both halves.
 constexpr int NST = KC == 256 ? 2 : FRR_NT_ST;  // TMEM holds two 64-column A stages at KC = 256
@@ -97,12 +87,9 @@ __host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
     return s;
 }
 
-#ifndef FRR_NT_ONEFULL
-#define FRR_NT_ONEFULL 1
-#endif
-// FRR_NT_ONEFULL: one "stage full" barrier per ring slot, arrived on by the 8
-// expansion warps and by the bulk copy (arrive + expect_tx)
-constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = FRR_NT_ONEFULL ? B_A_FULL : B_A_FULL + NST;
+// one "stage full" barrier per ring slot, arrived on by the 8 expansion warps
+// and by the bulk copy (arrive + expect_tx)
+constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = B_A_FULL;
 constexpr int B_S_EMPTY = B_B_FULL + NST, B_TM_FULL = B_S_EMPTY + NST, B_TM_EMPTY = B_TM_FULL + 2;
 static_assert(B_TM_EMPTY + 2 <= 30, "barrier slots");
 
@@ -143,23 +130,9 @@ __device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity) {
     }
 }
 
-// hardware-suspended wait (try_wait with a time hint): no issue slots spent
+// spin wait for the pipeline roles (suspend-hint and sleep variants measured no better)
 __device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
-#if FRR_NT_HWWAIT
-    const uint32_t a = smem_u32(b);
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity), "r"(100000)
-            : "memory");
-    } while (!ok);
-#else
     mbar_wait(b, parity);
-#endif
 }
 
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
@@ -199,8 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&bars[B_BITS_EMPTY + b], NEXP);
         }
         for (int s = 0; s < nst; s++) {
-            mbar_init(&bars[B_A_FULL + s], FRR_NT_ONEFULL ? NEXP + 1 : NEXP);
-            if (!FRR_NT_ONEFULL) mbar_init(&bars[B_B_FULL + s], 1);
+            mbar_init(&bars[B_A_FULL + s], NEXP + 1);
             mbar_init(&bars[B_S_EMPTY + s], 1);
         }
         for (int s = 0; s < 2; s++) {
@@ -274,13 +246,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint32_t w = src[q], wh = w >> 4;
 #pragma unroll
                         for (int b = 0; b < 8; b++) {
-#if FRR_NT_PRESHIFT
                             // bit 8j+b of w lands in byte j of register b with weight
                             // 2^(b&3); the B rows carry the compensating 2^(3-(b&3))
                             v[q * 8 + b] = (b < 4 ? w : wh) & (0x01010101u << (b & 3));
-#else
-                            v[q * 8 + b] = (w >> b) & 0x01010101u;  // see frr_kpos_bit
-#endif
                         }
                     }
                     if (!(FRR_NT_DEBUG & 2)) {
@@ -301,8 +269,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
         const double g = bal.g, cst = bal.cst;
         const int d = S.d;
-        // per-limb accumulators are bounded by n * 2^(3*PRESHIFT) * 128
-        const bool pair32 = (int64_t)S.n * (128 << (3 * FRR_NT_PRESHIFT)) * 257 < (1ll << 31);
+        // per-limb accumulators are bounded by n * 8 * 128 (pre-shifted rows)
+        const bool pair32 = (int64_t)S.n * (128 << 3) * 257 < (1ll << 31);
         uint32_t chunk_ctr = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             double racc[8];
@@ -328,7 +296,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int u = 0; u < 8; u++) {
                         const int j = j0 + u;
                         const double cc = j < d ? bal.cc[j] : 0.0;
-                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> (3 * FRR_NT_PRESHIFT)), g), cc);
+                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> 3), g), cc);
                         q[u] = __dmul_rn(delta, delta);
                     }
                     const int G = j0 >> 3;
@@ -416,13 +384,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int kc = 0; kc < S.nkc; kc++) {
                         const int st = m_s;
                         mbar_wait(&bars[B_A_FULL + st], m_ph);
-                        if (!FRR_NT_ONEFULL) mbar_wait(&bars[B_B_FULL + st], m_ph);
                         if (++m_s == nst) {
                             m_s = 0;
                             m_ph ^= 1;
                         }
                         tc_fence_after();
-#if FRR_NT_LEAN_ISSUE
                         // descriptor of stage st, K step ks = base descriptor + address offset
                         // (start address field: bits 0-13 in 16-byte units; shared
                         // addresses < 256 KB never carry out of it)
@@ -431,15 +397,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                         for (int ks = 0; ks < KC / 32; ks++)
                             tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), bd + (uint64_t)(ks * b_ks16), idesc, (kc | ks) != 0);
-#else
-                        const uint32_t at = tmem_base + (uint32_t)(2 * S.nc + st * (KC / 4));
-                        const uint32_t b0 = smem_u32(sB + (size_t)st * S.nc * KC);
-#pragma unroll
-                        for (int ks = 0; ks < KC / 32; ks++) {
-                            tc_mma_i8_ts(dt, at + (uint32_t)(ks * 8), umma_desc(b0 + ks * 2 * b_lbo, b_lbo, 128), idesc,
-                                         (kc | ks) != 0);
-                        }
-#endif
                         tc_commit(&bars[B_S_EMPTY + st]);
                     }
                     tc_commit(&bars[B_TM_FULL + tb]);
@@ -477,7 +434,7 @@ __global__ void k_prepare_limbs_nt(const int64_t* __restrict__ zq, NtShape S, in
             // pre-shifted rows: K offset r of a 32-group is expanded with weight
             // 2^((r>>2)&3), so its limbs encode z * 2^(3-((r>>2)&3)) (all
             // products carry 8; the epilogue divides the exact sum by 8)
-            int64_t z = zq[(size_t)k * S.d + j] * (FRR_NT_PRESHIFT ? (int64_t)(8 >> ((kk >> 2) & 3)) : 1);
+            int64_t z = zq[(size_t)k * S.d + j] * (int64_t)(8 >> ((kk >> 2) & 3));
             for (int q = 0; q <= l; q++) {
                 v = (int8_t)(z & 0xFF);
                 z = (z - v) >> 8;
