@@ -332,18 +332,18 @@ __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uin
                     uint64_t rr = xc + cbit;
                     uint64_t xn = (((rr ^ xc) >> 2) >> (__ffsll((long long)cbit) - 1)) | rr;
                     uint64_t mn = ~xn & fullmask;
-                    uint64_t diff = m ^ mn;
-                    while (diff) {
-                        int b = __ffsll((long long)diff) - 1;
-                        const int64_t* z = zq + (size_t)(n - 1 - b) * D;
-                        if ((mn >> b) & 1ull) {
+                    // the successor keeps the popcount: units leave and enter in
+                    // pairs, one (enter, leave) pair per iteration (no divergent
+                    // add/subtract paths)
+                    uint64_t add = mn & ~m, rem = m & ~mn;
+                    while (add) {
+                        const int ba = __ffsll((long long)add) - 1, br = __ffsll((long long)rem) - 1;
+                        const int64_t* za = zq + (size_t)(n - 1 - ba) * D;
+                        const int64_t* zr = zq + (size_t)(n - 1 - br) * D;
 #pragma unroll
-                            for (int j = 0; j < D; j++) S[j] += z[j];
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < D; j++) S[j] -= z[j];
-                        }
-                        diff &= diff - 1;
+                        for (int j = 0; j < D; j++) S[j] += za[j] - zr[j];
+                        add &= add - 1;
+                        rem &= rem - 1;
                     }
                     m = mn;
                 }
@@ -667,6 +667,7 @@ extern "C" int frr_exact_stats(const frr_balance_t* bal, uint64_t rank_lo, int64
     if (count <= 0) return FRR_OK;
     if (bal->n <= 64 && bal->d <= 16) {
         if (bal->d <= 4) return launch_exact_small<4>(bal, rank_lo, count, stats, stream);
+        if (bal->d <= 6) return launch_exact_small<6>(bal, rank_lo, count, stats, stream);  // C1/C4: d = 5
         if (bal->d <= 8) return launch_exact_small<8>(bal, rank_lo, count, stats, stream);
         return launch_exact_small<16>(bal, rank_lo, count, stats, stream);
     }
