@@ -89,15 +89,26 @@ __device__ __forceinline__ void build_table(uint64_t seed, const uint64_t* ids, 
     }
 }
 
+// Bit i of word w = unit 32w+i is treated (its entry is not FRR_CTL; every
+// other entry value is < 2^15, so "treated" is bit 15 clear).  Four 16-byte
+// loads per word; units >= n (table padding) read as 0.
 __device__ __forceinline__ uint32_t table_word(const uint16_t* lw, int n, int w) {
+    const uint4* src = reinterpret_cast<const uint4*>(lw + 32 * w);
     uint32_t word = 0;
-    int e0 = w * 32;
-#pragma unroll 8
-    for (int i = 0; i < 32; i++) {
-        int e = e0 + i;
-        if (e < n && lw[e] != FRR_CTL) word |= 1u << i;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const uint4 v = src[c];
+        const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t nb = ~x[j];  // bit 15: unit 2k treated, bit 31: unit 2k+1 treated
+            const int k = 4 * c + j;
+            word |= ((nb >> 15) & 1u) << (2 * k);
+            word |= (nb >> 31) << (2 * k + 1);
+        }
     }
-    return word;
+    const int valid = n - 32 * w;
+    return valid >= 32 ? word : word & ((1u << valid) - 1u);
 }
 
 // ------------------------------------------------------------- regeneration
