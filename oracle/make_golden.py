@@ -195,6 +195,25 @@ def gen_pairwise():
     np.savez_compressed(os.path.join(OUT, "pairwise.npz"), **out)
 
 
+def gen_sim():
+    """Synthetic-input helpers (bench.py:101-154): keyed normals, simulate_data
+    inputs (X, coefficients, noise streams), the cost model."""
+    from fastrr import bench as B
+
+    out = {}
+    for seed, stream, count in [(0, 0, 1), (7, 0, 1000), (7, 2, 999), (123, 5, 4096)]:
+        out[f"normals_{seed}_{stream}_{count}"] = B.normals_from_stream(seed, stream, count)
+    cfg = B.SimConfig(n=20, k=5)
+    X, obs, y = B.simulate_data(cfg, seed=3)
+    out["sim_X"], out["sim_bits"], out["sim_y"] = X.values, np.asarray(obs.bits), y
+    cfg2 = B.SimConfig(n=12, k=3, coef=np.array([1.0, -2.0, 0.5]), tau_true=2.0, noise_sd=0.1)
+    X2, obs2, y2 = B.simulate_data(cfg2, seed=11)
+    out["sim2_X"], out["sim2_bits"], out["sim2_y"] = X2.values, np.asarray(obs2.bits), y2
+    out["speedup"] = np.array([B.estimate_speedup(B.CostModel(0.5, 0.01, 2e-6, 64, 400.0, 10**8)),
+                               B.estimate_speedup(B.CostModel(0.0, 1.0, 1.0, 1, 1.0, 0))])
+    np.savez_compressed(os.path.join(OUT, "sim.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     print("reference fastrr", fastrr.__version__, "from", REF)
@@ -203,5 +222,6 @@ if __name__ == "__main__":
     gen_balance()
     gen_pools()
     gen_inference()
+    gen_sim()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
