@@ -187,7 +187,8 @@ int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t*
 int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t* total_draws_host, void* stream);
 /* Tensor-pipe ceiling for the int8 path: one CTA per SM issuing `iters` x 4
  * back-to-back tcgen05.mma.kind::i8 (M=128, N, K=32) into one TMEM
- * accumulator, A from shared memory (a_tmem = 0) or TMEM (1).
+ * accumulator, A from shared memory (a_tmem bit 0 clear) or TMEM (set);
+ * bit 1 set: random operand bytes instead of zeros.
  * *ops_host = 2*M*N*K*instructions (int8 ops) of the launch. */
 int frr_microbench_mma_i8(int N, int a_tmem, int64_t iters, int64_t* ops_host, void* stream);
 

@@ -633,8 +633,16 @@ __global__ void __launch_bounds__(128) k_microbench_mma(int N, int a_tmem, int64
     unsigned char* sB = smem + BM * 128;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (size_t)N * 128);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
-    for (int o = threadIdx.x; o < (BM + N) * 128 / 16; o += blockDim.x)
-        reinterpret_cast<uint4*>(smem)[o] = make_uint4(0, 0, 0, 0);
+    const bool rnd = (a_tmem & 2) != 0;  // random operand bytes instead of zeros
+    a_tmem &= 1;
+    for (int o = threadIdx.x; o < (BM + N) * 128 / 16; o += blockDim.x) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (rnd) {
+            const uint64_t h = frr_mix64((uint64_t)o), h2 = frr_mix64(h);
+            v = make_uint4((uint32_t)h, (uint32_t)(h >> 32), (uint32_t)h2, (uint32_t)(h2 >> 32));
+        }
+        reinterpret_cast<uint4*>(smem)[o] = v;
+    }
     fence_proxy_async();
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -648,6 +656,15 @@ __global__ void __launch_bounds__(128) k_microbench_mma(int N, int a_tmem, int64
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *slot;
+    if (rnd && a_tmem) {  // A stage (TMEM columns 256..287) with random bytes
+        uint32_t v[32];
+        for (int c = 0; c < 32; c++) v[c] = (uint32_t)frr_mix64((uint64_t)(threadIdx.x * 32 + c + 12345));
+        tc_st32(tmem + ((uint32_t)((threadIdx.x >> 5) * 32) << 16) + 256, v);
+        tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     if (threadIdx.x == 0) {
         const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(N / 8) * 128;
         const uint32_t idesc = idesc_i8(BM, N);

@@ -52,3 +52,7 @@ int frr_mc_stats_nt(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_
     return nt256::fits(bal->n, bal->d, bal->n_limbs) ? nt256::mc_stats(bal, seed, lo, count, stats, stream)
                                                       : nt128::mc_stats(bal, seed, lo, count, stats, stream);
 }
+
+#if FRR_NT_TIMING
+extern "C" int frr_debug_nt_waits(unsigned long long* host16) { return nt256::debug_waits(host16); }
+#endif

@@ -19,13 +19,57 @@ constexpr int KC = FRR_NT_KC;  // K bytes per stage: this instantiation's (128 o
 #ifndef FRR_NT_DEBUG
 #define FRR_NT_DEBUG 0
 #endif
+// wait-time accounting (debug builds, FRR_NT_TIMING=1; read back with
+// frr_debug_nt_waits for the 256-byte-stage instantiation)
+#ifndef FRR_NT_TIMING
+#define FRR_NT_TIMING 0
+#endif
+#if FRR_NT_TIMING
+__device__ unsigned long long g_nt_waits[16];
+#define NTW(slot, ...)                         \
+    do {                                       \
+        const long long t0_ = clock64();       \
+        __VA_ARGS__;                           \
+        wacc[slot] += clock64() - t0_;         \
+    } while (0)
+#else
+#define NTW(slot, ...) \
+    do {               \
+        __VA_ARGS__;   \
+    } while (0)
+#endif
 // K-stage ring: stage s = A chunk s in TMEM + B chunk s in shared memory, one
 // "stage consumed" barrier (a single tcgen05.commit) releases both halves.
 constexpr int NST = KC == 256 ? 2 : FRR_NT_ST;  // TMEM holds two 64-column A stages at KC = 256
 constexpr int NFY = FRR_NT_NFY;
 constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
-constexpr int W_EXP0 = 4, W_TMA = W_EXP0 + NEXP, W_MMA = W_TMA + 1, W_FY0 = W_MMA + 1;
-constexpr int NWARPS = W_FY0 + NFY;
+// Warp roles (the scheduler favours higher warp ids; the epilogue is the
+// measured bottleneck of this kernel, so it gets the highest ones).
+#ifndef FRR_NT_LAYOUT
+#define FRR_NT_LAYOUT 2
+#endif
+#if FRR_NT_LAYOUT == 2
+// expansion 0..NEXP-1, generators, bulk copy, MMA, then the epilogue on the
+// highest ids (4-aligned: warp % 4 is its TMEM lane quadrant)
+constexpr int W_EXP0 = 0, W_FY0 = NEXP;
+__host__ __device__ constexpr int w_tma(int nfy) { return W_FY0 + nfy; }
+__host__ __device__ constexpr int w_mma(int nfy) { return W_FY0 + nfy + 1; }
+__host__ __device__ constexpr int w_epi0(int nfy) { return (W_FY0 + nfy + 2 + 3) & ~3; }
+__host__ __device__ constexpr int n_warps(int nfy) { return w_epi0(nfy) + 4; }
+#elif FRR_NT_LAYOUT == 1
+constexpr int W_EXP0 = 4, W_FY0 = W_EXP0 + NEXP;
+__host__ __device__ constexpr int w_tma(int nfy) { return W_FY0 + nfy; }
+__host__ __device__ constexpr int w_mma(int nfy) { return W_FY0 + nfy + 1; }
+__host__ __device__ constexpr int w_epi0(int) { return 0; }
+__host__ __device__ constexpr int n_warps(int nfy) { return W_FY0 + nfy + 2; }
+#else
+constexpr int W_EXP0 = 4, W_FY0 = W_EXP0 + NEXP + 2;
+__host__ __device__ constexpr int w_tma(int) { return W_EXP0 + NEXP; }
+__host__ __device__ constexpr int w_mma(int) { return W_EXP0 + NEXP + 1; }
+__host__ __device__ constexpr int w_epi0(int) { return 0; }
+__host__ __device__ constexpr int n_warps(int nfy) { return W_FY0 + nfy; }
+#endif
+constexpr int NWARPS = n_warps(NFY);
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int DJ = 32;  // covariates per N-chunk
 constexpr int MAX_LEAVES = 1024;
@@ -161,6 +205,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int rowstride = S.kw + 4;
     const int nst = min(NST, (512 - 2 * S.nc) / (KC / 4));  // ring stages whose A fits in TMEM
     const int c_nfy = FULL ? NFY : S.nfy, c_nbits = FULL ? 2 : S.nbits;
+#if FRR_NT_TIMING
+    long long wacc[16] = {0};
+    const long long tstart = clock64();
+#endif
 
     for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
     __syncthreads();
@@ -182,6 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
+    const int W_TMA = w_tma(c_nfy), W_MMA = w_mma(c_nfy), W_EPI0 = w_epi0(c_nfy);
     if (warp == W_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -191,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp >= W_FY0) {
+    if (warp >= W_FY0 && warp < W_FY0 + c_nfy) {
         // ===================================================== generators
         const int fyw = warp - W_FY0;
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
@@ -199,7 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i % c_nbits;
-            mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1);
+            NTW(0, mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1));
             uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
             for (int r = fyw; r < BM; r += c_nfy) {
                 const int64_t c = tile * BM + r;
@@ -228,12 +277,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t a_ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i % c_nbits;
-            mbar_wait_hw(&bars[B_BITS_FULL + buf], (i / c_nbits) & 1);
+            NTW(1, mbar_wait_hw(&bars[B_BITS_FULL + buf], (i / c_nbits) & 1));
             const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
             for (int c = 0; c < S.nch; c++) {
                 for (int kc = 0; kc < S.nkc; kc++) {
                     const int s = a_s;
-                    mbar_wait_hw(&bars[B_S_EMPTY + s], a_ph ^ 1);
+                    NTW(2, mbar_wait_hw(&bars[B_S_EMPTY + s], a_ph ^ 1));
                     if (++a_s == nst) {
                         a_s = 0;
                         a_ph ^= 1;
@@ -263,10 +312,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars[B_BITS_EMPTY + buf]);
         }
-    } else if (warp < 4) {
+    } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ================================================ streaming epilogue
-        const int r = threadIdx.x;  // tile row == TMEM lane
-        const uint32_t tl = tmem_base + ((uint32_t)(warp * 32) << 16);
+        const int r = threadIdx.x - W_EPI0 * 32;  // tile row == TMEM lane
+        const uint32_t tl = tmem_base + ((uint32_t)((warp - W_EPI0) * 32) << 16);
         const double g = bal.g, cst = bal.cst;
         const int d = S.d;
         // per-limb accumulators are bounded by n * 8 * 128 (pre-shifted rows)
@@ -281,7 +330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             bool done = false;
             for (int c = 0; c < S.nch; c++, chunk_ctr++) {
                 const int tb = chunk_ctr & 1;
-                mbar_wait_lazy(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1);
+                NTW(3, mbar_wait_lazy(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1));
                 tc_fence_after();
                 const uint32_t cb = tl + (uint32_t)(tb * S.nc);
                 for (int g4 = 0; g4 < DJ / 8; g4++) {
@@ -350,7 +399,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int c = 0; c < S.nch; c++) {
                     for (int kc = 0; kc < S.nkc; kc++) {
                         const int s = bs;
-                        mbar_wait_hw(&bars[B_S_EMPTY + s], bph ^ 1);
+                        NTW(4, mbar_wait_hw(&bars[B_S_EMPTY + s], bph ^ 1));
                         if (++bs == nst) {
                             bs = 0;
                             bph ^= 1;
@@ -378,12 +427,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int c = 0; c < S.nch; c++, chunk_ctr++) {
                     const int tb = chunk_ctr & 1;
-                    mbar_wait(&bars[B_TM_EMPTY + tb], ((chunk_ctr >> 1) & 1) ^ 1);
+                    NTW(5, mbar_wait(&bars[B_TM_EMPTY + tb], ((chunk_ctr >> 1) & 1) ^ 1));
                     tc_fence_after();
                     const uint32_t dt = tmem_base + (uint32_t)(tb * S.nc);
                     for (int kc = 0; kc < S.nkc; kc++) {
                         const int st = m_s;
-                        mbar_wait(&bars[B_A_FULL + st], m_ph);
+                        NTW(6, mbar_wait(&bars[B_A_FULL + st], m_ph));
                         if (++m_s == nst) {
                             m_s = 0;
                             m_ph ^= 1;
@@ -405,6 +454,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
 
+#if FRR_NT_TIMING
+    {
+        const int role = warp == W_MMA ? 11 : warp == W_TMA ? 12
+                       : warp >= W_EPI0 && warp < W_EPI0 + 4 ? 10
+                       : warp >= W_EXP0 && warp < W_EXP0 + NEXP ? 9 : 8;
+        wacc[role] += clock64() - tstart;
+        if (lane == 0)
+            for (int k = 0; k < 16; k++)
+                if (wacc[k]) atomicAdd(&g_nt_waits[k], (unsigned long long)wacc[k]);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == W_MMA) {
@@ -481,8 +541,18 @@ int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count
     if ((rc = frr_prepare_kernel(kern, P.total))) return rc;
     int64_t ntiles = frr_cdiv(count, BM);
     int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
-    kern<<<grid, (W_FY0 + S.nfy) * 32, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
+    kern<<<grid, n_warps(S.nfy) * 32, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
     return frr_check_launch("k_mc_stats_nt");
 }
+
+#if FRR_NT_TIMING
+int debug_waits(unsigned long long* host16) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host16, g_nt_waits, sizeof(unsigned long long) * 16);
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_nt_waits, z, sizeof(z));
+    return 0;
+}
+#endif
 
 }  // namespace FRR_NT_NS

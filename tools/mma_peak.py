@@ -12,8 +12,8 @@ sys.path.insert(0, ROOT)
 from paper_2501_07642_b200 import _native as N  # noqa: E402
 
 res = {}
-for a_tmem in (0, 1):
-    for n in (64, 128, 192, 256):
+for a_tmem in (0, 1, 2, 3):
+    for n in (128, 192, 256):
         ops = ctypes.c_int64(0)
         best = 0.0
         for _ in range(3):
@@ -23,6 +23,7 @@ for a_tmem in (0, 1):
             e1.record()
             torch.cuda.synchronize()
             best = max(best, ops.value / (e0.elapsed_time(e1) / 1e3))
-        res[f"N{n}_{'tmemA' if a_tmem else 'smemA'}"] = best / 1e12
-        print(f"N={n} A={'tmem' if a_tmem else 'smem'}: {best / 1e12:.0f} TOP/s int8", flush=True)
+        tag = f"N{n}_{'tmemA' if a_tmem & 1 else 'smemA'}_{'random' if a_tmem & 2 else 'zeros'}"
+        res[tag] = best / 1e12
+        print(f"{tag}: {best / 1e12:.0f} TOP/s int8", flush=True)
 print(json.dumps(res))
