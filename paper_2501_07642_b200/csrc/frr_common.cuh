@@ -277,11 +277,12 @@ __device__ __forceinline__ uint32_t frr_pack_word(const uint16_t* lw, int w) {
         const int cc = (c + w) & 3;  // rotate 16-byte chunks: conflict-free across lanes
         const uint4 v = src[cc];
         const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+        // component i = 4 cc + j contributes (~x & 0x80008000) >> i: compile-time
+        // shifts by j inside the chunk, one runtime shift by 4 cc per chunk
+        uint32_t part = 0;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int i = 4 * cc + j;  // component index (units 32w+2i, 32w+2i+1)
-            acc |= (~x[j] & 0x80008000u) >> i;
-        }
+        for (int j = 0; j < 4; j++) part |= ~(x[j] >> j) & (0x80008000u >> j);
+        acc |= part >> (4 * cc);
     }
     return acc;
 }
