@@ -68,7 +68,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("FRR_CLOCK_MS", "200")], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         return self
