@@ -3,8 +3,9 @@
 // Replaces generation.py:185-204 (_pass1_stats) = keys.py:177-208 feeding
 // balance.py:93-105 for mid-size d.  Per 128-candidate tile:
 //
-//   FY warps (10)   key -> assignment in a per-warp smem table (frr_warp_fy),
-//                   packed to a bit row of the tile (never leaves the SM)
+//   FY warps (26;   key -> assignment in a per-warp smem table (frr_warp_fy),
+//   fewer at large  packed to a bit row of the tile (never leaves the SM);
+//   n)              up to 3 bit-row tile buffers
 //   tile warps (4)  expand bit rows to int8 0/1 A-operand K-chunks in the
 //                   tcgen05 K-major canonical layout; later the epilogue
 //   TMA warp        cp.async.bulk of the pre-tiled int8-limb B operand

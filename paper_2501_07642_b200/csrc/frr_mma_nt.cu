@@ -9,11 +9,11 @@
 // combine stack driven by a plan built once per CTA), so the statistic stays
 // bit-identical for any d.
 //
-// Warp roles: 0-3 epilogue (TMEM lane quadrants), 4-11 A-operand expansion
-// (bit rows -> int8 K-chunks written straight into TMEM with tcgen05.st, once
-// per N-chunk pass; the MMA reads A from TMEM, so only the B stream uses shared
-// memory bandwidth), then the bulk-copy warp for the int8-limb B chunks, the
-// tcgen05.mma issuer and the Fisher-Yates generator warps.
+// Warp roles (frr_mma_nt_body.cuh): A-operand expansion (bit rows -> int8
+// K-chunks written straight into TMEM with tcgen05.st, once per N-chunk pass;
+// one LOP3 per register because the B rows are pre-shifted), the Fisher-Yates
+// generators, the bulk-copy warp for the int8-limb B chunks, the tcgen05.mma
+// issuer, and the epilogue (4 warps, TMEM lane quadrants) on the highest ids.
 // TMEM columns: [0, 2 NC) two accumulators, then nst A stages of KC/4 columns.
 #include <cuda_runtime.h>
 
