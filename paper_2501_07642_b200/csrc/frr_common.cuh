@@ -73,9 +73,10 @@ __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s) {
     const uint32_t llo = mlo * ylo;
     const uint32_t lhi = __umulhi(mlo, ylo) + mhi * ylo + mlo * yhi;
     // result = floor(low * b / 2^64) = hi32(lhi * b + umulhi(llo, b))
-    uint32_t rlo, rhi;
-    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(rlo), "=r"(rhi) : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)));
-    (void)rlo;
+    uint32_t rhi;  // the low word of the sum only feeds the carry
+    asm("{\n\t.reg .u32 rlo;\n\tmad.lo.cc.u32 rlo, %1, %2, %3;\n\tmadc.hi.u32 %0, %1, %2, 0;\n\t}"
+        : "=r"(rhi)
+        : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)));
     return rhi;
 }
 
