@@ -260,7 +260,11 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("k_mc_stats_mma_bytes_per_launch")
-    launches_per_step = 1 + 1 + 16 + 3 + (0 if world == 1 else 1)
+    # libfrr kernels per step: pass 1 (1); sampled bound: init + 8 x (hist, pick)
+    # (17); narrowing: init + tile counts, scan, compact (4); radix select on the
+    # narrowed set + final compaction (17 + 3); + the (less, equal) count at
+    # world > 1 (cf. profiles/r01d_launch_shares.txt)
+    launches_per_step = 1 + 17 + 4 + 20 + (0 if world == 1 else 1)
     draw_peak = _draw_peak(N)
     issue = None
     ip = os.path.join(ROOT, "profiles", "issue.json")
