@@ -1,0 +1,121 @@
+"""Multi-rank pool construction (NCCL on the GPU path) over gloo on CPU:
+generation._Pass1's candidate sharding, the global select and the pool
+assembly at world sizes 2 and 3 must give exactly the world-size-1 pool, and
+_PoolStats' rank-ordered gather of the test statistics must reassemble them.
+The per-rank GPU compute (pass-1 statistics, select kernels, exact rows) is
+replaced by the C oracle / numpy checker ops; the orchestration under test
+is the product's."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import paper_2501_07642_b200 as frr
+from paper_2501_07642_b200 import generation as G
+from paper_2501_07642_b200._select import select_k_smallest
+from paper_2501_07642_b200.inference import _PoolStats
+from select_ops import NumpySelectOps
+
+
+def _patch_compute(setattr_=setattr):
+    def mc_stats(kernel, design, lo, count, out=None):
+        bal = O.Balance(kernel._zq, kernel._inv_scale_sq)
+        return torch.from_numpy(O.c_mc_stats(bal, design.n_treated, design.root_seed, lo, count, threads=1))
+
+    def exact_stats(kernel, design, lo, count, out=None):
+        bal = O.Balance(kernel._zq, kernel._inv_scale_sq)
+        return torch.from_numpy(O.c_exact_stats(bal, design.n_treated, lo, count, threads=1))
+
+    def select(stats, lo, k, comm):
+        idx, val, thr = select_k_smallest(stats, lo, k, NumpySelectOps(), comm)
+        return idx.numpy(), val.numpy(), thr
+
+    setattr_(G, "mc_stats_device", mc_stats)
+    setattr_(G, "exact_stats_device", exact_stats)
+    setattr_(G, "_select_device", select)
+    setattr_(G, "exact_rows_device", lambda ranks, n, t: torch.from_numpy(O.c_exact_rows(ranks, n, t)))
+
+
+CASES = {
+    "mc": (np.random.default_rng(21).standard_normal((12, 3)),
+           dict(n_units=12, n_treated=6, accept_prob=0.05, max_draws=4001, batch_size=97, root_seed=21)),
+    "mc_ties": (np.random.default_rng(3).standard_normal((10, 1)),
+                dict(n_units=10, n_treated=5, accept_prob=0.3, max_draws=1000, batch_size=25,
+                     precision_mode="diagonal", root_seed=3)),
+    "exact": (np.random.default_rng(102).standard_normal((14, 3)),
+              dict(n_units=14, n_treated=7, accept_prob=0.03, mode="exact")),
+}
+
+
+def _build(name):
+    X, kw = CASES[name]
+    design = frr.DesignSpec(**kw)
+    pool = frr.generate_pool(X, design)
+    return (pool.accepted_indices, pool.stats, pool.threshold_value,
+            None if pool.assignments is None else pool.assignments, None if pool.keys is None else pool.keys)
+
+
+def _worker(rank, world, port, name, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _patch_compute()
+        out[rank] = _build(name)
+    finally:
+        dist.destroy_process_group()
+
+
+def _gather_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_07642_b200._select import TorchComm
+
+        m = 1001
+        a = np.arange(m, dtype=np.float64) * 0.5
+        b = -np.arange(m, dtype=np.float64)
+        lo, hi = m * rank // world, m * (rank + 1) // world
+        match = torch.tensor([1 if rank == world - 1 else 0], dtype=torch.int32)
+        ga, gb, gm = _PoolStats._gather(TorchComm(), torch.from_numpy(a[lo:hi].copy()),
+                                        torch.from_numpy(b[lo:hi].copy()), match)
+        out[rank] = (ga.numpy(), gb.numpy(), int(gm.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("name,world", [("mc", 2), ("mc_ties", 3), ("exact", 2)])
+def test_sharded_pool_equals_single_rank(name, world, monkeypatch):
+    _patch_compute(monkeypatch.setattr)  # restored after the test
+    want = _build(name)  # world size 1 (no process group in this process)
+    with mp.Manager() as man:
+        out = man.dict()
+        mp.spawn(_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
+        results = dict(out)
+    for r in range(world):
+        got = results[r]
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]) and got[2] == want[2]
+        for g, w in zip(got[3:], want[3:]):
+            assert (g is None and w is None) or np.array_equal(g, w)
+
+
+def test_pool_stats_gather_rank_order():
+    world = 3
+    with mp.Manager() as man:
+        out = man.dict()
+        mp.spawn(_gather_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        results = dict(out)
+    for r in range(world):
+        a, b, match = results[r]
+        assert np.array_equal(a, np.arange(1001) * 0.5) and np.array_equal(b, -np.arange(1001.0)) and match == 1
