@@ -175,31 +175,51 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const uint64_t* __restric
                                                        double* stat_out) {
     const uint64_t T = st->prefix;
     const int64_t quota = *tie_quota;
-    int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;  // thread-contiguous run
+    // coalesced tile load through shared memory (row stride kPer+1 words:
+    // 2-way bank conflicts), then thread-contiguous runs of kPer elements
+    __shared__ uint64_t s_tile[kCThreads * (kPer + 1)];
+    const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+        const int e = j * kCThreads + threadIdx.x;  // element of the tile
+        const int64_t i = tile0 + e;
+        s_tile[(e / kPer) * (kPer + 1) + e % kPer] = i < m ? bits[i] : ~0ull;
+    }
+    __syncthreads();
+    int64_t base = tile0 + (int64_t)threadIdx.x * kPer;  // thread-contiguous run
     uint64_t v[kPer];
     int lt = 0, eq = 0;
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
-        int64_t i = base + j;
-        v[j] = i < m ? bits[i] : ~0ull;
+        v[j] = s_tile[threadIdx.x * (kPer + 1) + j];
         lt += v[j] < T;
         eq += v[j] == T;
     }
-    // block exclusive scan of (lt, eq) in thread order
-    __shared__ int s_lt[kCThreads], s_eq[kCThreads];
-    s_lt[threadIdx.x] = lt;
-    s_eq[threadIdx.x] = eq;
-    __syncthreads();
-    for (int o = 1; o < kCThreads; o <<= 1) {
-        int a = threadIdx.x >= o ? s_lt[threadIdx.x - o] : 0;
-        int b = threadIdx.x >= o ? s_eq[threadIdx.x - o] : 0;
-        __syncthreads();
-        s_lt[threadIdx.x] += a;
-        s_eq[threadIdx.x] += b;
-        __syncthreads();
+    // block exclusive scan of (lt, eq) in thread order: warp shuffles, then
+    // the 8 warp totals (one barrier)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int il = lt, ie = eq;  // inclusive within the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(FRR_FULL, il, o), b = __shfl_up_sync(FRR_FULL, ie, o);
+        if (lane >= o) {
+            il += a;
+            ie += b;
+        }
     }
-    int64_t lrank = ws[2 * blockIdx.x] + s_lt[threadIdx.x] - lt;
-    int64_t erank = ws[2 * blockIdx.x + 1] + s_eq[threadIdx.x] - eq;
+    __shared__ int s_wl[kCThreads / 32], s_we[kCThreads / 32];
+    if (lane == 31) {
+        s_wl[wid] = il;
+        s_we[wid] = ie;
+    }
+    __syncthreads();
+    int bl = 0, be = 0;
+    for (int w = 0; w < wid; w++) {
+        bl += s_wl[w];
+        be += s_we[w];
+    }
+    int64_t lrank = ws[2 * blockIdx.x] + bl + il - lt;
+    int64_t erank = ws[2 * blockIdx.x + 1] + be + ie - eq;
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
         bool less = v[j] < T, tie = v[j] == T;

@@ -22,3 +22,11 @@ for _ in range(2):
            N.stream_ptr())
 torch.cuda.synchronize()
 print("ok")
+# one 512-point tau grid over the m keys (k_tau_counts)
+taus = torch.linspace(-1.0, 1.0, 512, dtype=torch.float64, device="cuda")
+rhs = torch.full((512,), 0.5, dtype=torch.float64, device="cuda")
+counts = torch.empty(512, dtype=torch.int64, device="cuda")
+for _ in range(2):
+    N.call("frr_tau_counts", N.ptr(a), N.ptr(b), m, N.ptr(taus), N.ptr(rhs), 512, N.ptr(counts), N.stream_ptr())
+torch.cuda.synchronize()
+print("ok tau")
