@@ -132,3 +132,43 @@ def test_tensor_core_path_is_used_for_c2_shape():
     kern = frr.precompute_precision(X, "exact")._kernel
     os.environ.pop("FRR_MC_PATH", None)
     assert kern.wants_tensor_cores() and kern.n_limbs == 6
+
+
+def test_integration_md_ctypes_stub():
+    """The binding INTEGRATION.md shows a fastrr maintainer (raw ctypes over
+    include/frr.h, no package code on the call path) gives the package's
+    statistics bit for bit."""
+    import ctypes
+
+    import torch
+
+    from paper_2501_07642_b200 import _native as N
+
+    lib = ctypes.CDLL(N.load_library()._name)
+
+    class frr_balance_t(ctypes.Structure):
+        _fields_ = [("n", ctypes.c_int32), ("d", ctypes.c_int32), ("t", ctypes.c_int32),
+                    ("n_limbs", ctypes.c_int32), ("zq", ctypes.c_void_p), ("colsum", ctypes.c_void_p),
+                    ("cc", ctypes.c_void_p), ("limbs", ctypes.c_void_p),
+                    ("g", ctypes.c_double), ("cst", ctypes.c_double)]
+
+    lib.frr_mc_stats.argtypes = [ctypes.POINTER(frr_balance_t), ctypes.c_uint64, ctypes.c_uint64,
+                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.frr_last_error.restype = ctypes.c_char_p
+
+    X = np.random.default_rng(7).standard_normal((300, 12))
+    design = frr.DesignSpec(300, 150, accept_prob=0.01, max_draws=20_000, root_seed=99)
+    kernel = frr.precompute_precision(X, "exact")._kernel
+    t, n = design.n_treated, kernel.n_units
+    nc = n - t
+    zq = torch.from_numpy(kernel._zq.astype("int64")).cuda()
+    colsum = torch.from_numpy(kernel._colsum.astype("int64")).cuda()
+    cc = torch.from_numpy(kernel._colsum * (1.0 / nc)).cuda()
+    bal = frr_balance_t(n, zq.shape[1], t, 0, zq.data_ptr(), colsum.data_ptr(), cc.data_ptr(), None,
+                        1.0 / t + 1.0 / nc, (t * nc / n) * kernel._inv_scale_sq)
+    out = torch.empty(design.max_draws, dtype=torch.float64, device="cuda")
+    rc = lib.frr_mc_stats(ctypes.byref(bal), design.root_seed, 0, design.max_draws, out.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, lib.frr_last_error()
+    want = G.mc_stats_device(kernel, design, 0, design.max_draws).cpu().numpy()
+    assert bits_equal(out.cpu().numpy(), want)
