@@ -1,0 +1,69 @@
+"""Full-size parity runs: every statistic of the C2 workload
+(1e8 Monte Carlo candidates) and of C4 (2.33e9 exact ranks, optional) from
+the GPU path compared bit for bit with the C oracle (test infrastructure,
+multi-threaded on the host), and the accepted pools compared with the
+oracle's stable selection.
+
+    python tools/full_parity.py c2 [c4] > result.json"""
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import oracle as O  # noqa: E402
+
+import paper_2501_07642_b200 as frr  # noqa: E402
+from paper_2501_07642_b200 import generation as G  # noqa: E402
+
+
+def run(name, X, design, oracle_stats, chunk):
+    t0 = time.perf_counter()
+    pool = frr.generate_pool(X, design)
+    t_pool = time.perf_counter() - t0
+    kern = frr.precompute_precision(X, design.precision_mode)._kernel
+    M = pool.n_candidates
+    mism, first_bad = 0, None
+    t0 = time.perf_counter()
+    want_all = np.empty(M, dtype=np.float64)
+    for lo in range(0, M, chunk):
+        c = min(chunk, M - lo)
+        gpu = (G.mc_stats_device if design.mode == "monte_carlo" else G.exact_stats_device)(kern, design, lo, c)
+        got = gpu.cpu().numpy()
+        want = oracle_stats(lo, c)
+        want_all[lo:lo + c] = want
+        bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+        if bad.size and first_bad is None:
+            first_bad = int(lo + bad[0])
+        mism += int(bad.size)
+    t_cmp = time.perf_counter() - t0
+    acc, thr = O.c_select(want_all, design.accept_prob)
+    return {"config": name, "candidates": M, "stat_mismatches": mism, "first_mismatch": first_bad,
+            "accepted": int(pool.n_accepted), "accepted_equal": bool(np.array_equal(pool.accepted_indices, acc)),
+            "accepted_stats_equal": bool(np.array_equal(pool.stats, want_all[acc])),
+            "threshold_equal": pool.threshold_value == thr, "gpu_pool_s": t_pool, "oracle_compare_s": t_cmp}
+
+
+def c2():
+    X = np.random.default_rng(2).standard_normal((1000, 64))
+    design = frr.DesignSpec(1000, 500, accept_prob=1e-3, max_draws=10**8, batch_size=10_000, root_seed=42)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    return run("C2 full (1e8 MC draws)", X, design, lambda lo, c: O.c_mc_stats(bal, 500, 42, lo, c), 10**7)
+
+
+def c4():
+    X = np.random.default_rng(4).standard_normal((34, 5))
+    design = frr.DesignSpec(34, 17, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    return run("C4 full (2.33e9 exact ranks)", X, design, lambda lo, c: O.c_exact_stats(bal, 17, lo, c), 2 * 10**8)
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:] or ["c2"]:
+        print(json.dumps({"c2": c2, "c4": c4}[name]()), flush=True)
