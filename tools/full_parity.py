@@ -1,10 +1,11 @@
 """Full-size parity runs: every statistic of the C2 workload
-(1e8 Monte Carlo candidates) and of C4 (2.33e9 exact ranks, optional) from
+(1e8 Monte Carlo candidates), of C4 (2.33e9 exact ranks) and every C5 test
+statistic (1e6 keys) from
 the GPU path compared bit for bit with the C oracle (test infrastructure,
 multi-threaded on the host), and the accepted pools compared with the
 oracle's stable selection.
 
-    python tools/full_parity.py c2 [c4] > result.json"""
+    python tools/full_parity.py c2 [c4] [c5] > result.json"""
 import json
 import math
 import os
@@ -64,6 +65,36 @@ def c4():
     return run("C4 full (2.33e9 exact ranks)", X, design, lambda lo, c: O.c_exact_stats(bal, 17, lo, c), 2 * 10**8)
 
 
+def c5(m=10**6):
+    """C5 test statistics of all 1e6 keys (n=5000): a = difference in means of
+    every regenerated assignment, b from the popcounts, and the p-value, against
+    the oracle's regeneration + numpy-order masked sums."""
+    from paper_2501_07642_b200.inference import _PoolStats
+
+    keys = np.column_stack([np.full(m, 5, dtype=np.uint64), 997 * np.arange(m, dtype=np.uint64)])
+    pool = frr.RandomizationPool(
+        design=frr.DesignSpec(5000, 2500, accept_prob=1.0, max_draws=m * 997, batch_size=997, root_seed=5),
+        stats=np.zeros(m), threshold_value=0.0, n_candidates=m * 997, accepted_indices=997 * np.arange(m), keys=keys)
+    X = np.random.default_rng(5).standard_normal((5000, 64))
+    obs = frr.batch_assignments(5, np.array([0], dtype=np.uint64), 5000, 2500)[0]
+    rng = np.random.default_rng(5)
+    y = X @ rng.standard_normal(64) + 1.0 * obs + 0.5 * rng.standard_normal(5000)
+    ps = _PoolStats(pool, obs, y)
+    a = ps.a.cpu().numpy()
+    res = frr.randomization_pvalue(obs, y, pool)
+    want = np.empty(m, dtype=np.float64)
+    t0 = time.perf_counter()
+    for lo in range(0, m, 20_000):
+        rows = O.c_batch_assign(5, keys[lo:lo + 20_000, 1], 5000, 2500)
+        want[lo:lo + rows.shape[0]] = O.c_dim_rows(rows, y, 2500)
+    tau_obs = float(O.c_dim_rows(np.asarray(obs, dtype=np.int8).reshape(1, -1), y, 2500)[0])
+    p_want = float(np.count_nonzero(np.abs(want) >= abs(tau_obs))) / m
+    return {"config": "C5 full (1e6 keys, n=5000)", "keys": m,
+            "a_mismatches": int(np.count_nonzero(a.view(np.uint64) != want.view(np.uint64))),
+            "tau_obs_equal": ps.tau_obs == tau_obs, "p_value": res.p_value, "p_value_equal": res.p_value == p_want,
+            "oracle_s": time.perf_counter() - t0}
+
+
 if __name__ == "__main__":
     for name in sys.argv[1:] or ["c2"]:
-        print(json.dumps({"c2": c2, "c4": c4}[name]()), flush=True)
+        print(json.dumps({"c2": c2, "c4": c4, "c5": c5}[name]()), flush=True)
