@@ -65,6 +65,39 @@ def c4():
     return run("C4 full (2.33e9 exact ranks)", X, design, lambda lo, c: O.c_exact_stats(bal, 17, lo, c), 2 * 10**8)
 
 
+def c3():
+    """C3 at full size (1e8 draws, n=2000, d=1024): the oracle cannot recompute
+    all 1e8 statistics, so it recomputes every accepted one, the 2000 ranks
+    around the threshold and 1e6 random draws; the pool must equal the
+    selection over the GPU statistics."""
+    X = np.random.default_rng(3).standard_normal((2000, 1024))
+    M = 10**8
+    design = frr.DesignSpec(2000, 1000, accept_prob=1e-4, max_draws=M, batch_size=10_000, root_seed=43,
+                            precision_mode="ridge")
+    t0 = time.perf_counter()
+    pool = frr.generate_pool(X, design)
+    t_pool = time.perf_counter() - t0
+    kern = frr.precompute_precision(X, "ridge")._kernel
+    st = G.mc_stats_device(kern, design, 0, M).cpu().numpy()
+    k = G._accepted_count(1e-4, M)
+    order = np.argsort(st, kind="stable")
+    acc = np.sort(order[:k])
+    rng = np.random.default_rng(31)
+    idx = np.unique(np.concatenate([order[: k + 1000], rng.integers(0, M, size=1_000_000)]))
+    bal = O.balance_setup(X, O.precision(X, "ridge"))
+    t0 = time.perf_counter()
+    want = np.empty(idx.shape[0], dtype=np.float64)
+    for lo in range(0, idx.shape[0], 5000):
+        rows = O.c_batch_assign(43, idx[lo:lo + 5000].astype(np.uint64), 2000, 1000)
+        want[lo:lo + rows.shape[0]] = O.c_stats_rows(bal, rows, 1000)
+    return {"config": "C3 full (1e8 MC draws, n=2000, d=1024)", "candidates": M, "checked": int(idx.shape[0]),
+            "stat_mismatches": int(np.count_nonzero(st[idx].view(np.uint64) != want.view(np.uint64))),
+            "accepted": int(pool.n_accepted), "accepted_equal": bool(np.array_equal(pool.accepted_indices, acc)),
+            "accepted_stats_equal": bool(np.array_equal(pool.stats, st[acc])),
+            "threshold_equal": bool(pool.threshold_value == st[order[k - 1]]), "gpu_pool_s": t_pool,
+            "oracle_s": time.perf_counter() - t0}
+
+
 def c5(m=10**6):
     """C5 test statistics of all 1e6 keys (n=5000): a = difference in means of
     every regenerated assignment, b from the popcounts, and the p-value, against
@@ -97,4 +130,4 @@ def c5(m=10**6):
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or ["c2"]:
-        print(json.dumps({"c2": c2, "c4": c4, "c5": c5}[name]()), flush=True)
+        print(json.dumps({"c2": c2, "c3": c3, "c4": c4, "c5": c5}[name]()), flush=True)
