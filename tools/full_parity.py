@@ -7,13 +7,11 @@ oracle's stable selection.
 
     python tools/full_parity.py c2 [c4] [c5] > result.json"""
 import json
-import math
 import os
 import sys
 import time
 
 import numpy as np
-import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
