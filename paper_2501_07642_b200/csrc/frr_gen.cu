@@ -284,24 +284,28 @@ __global__ void __launch_bounds__(kPlanThreads) k_stats_generic(frr_balance_t ba
 // then the complement-Gosper successor (unit i <-> bit n-1-i, lex order ==
 // decreasing mask) with an incremental exact S.  Results are transposed
 // through shared memory for coalesced stores.
-constexpr int kRun = 32;
+#ifndef FRR_KRUN
+#define FRR_KRUN 32
+#endif
+constexpr int kRun = FRR_KRUN;
 
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uint64_t rank_lo, int64_t count,
                                                           double* out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = bal.n, t = bal.t, d = bal.d;
-    uint64_t* binom = reinterpret_cast<uint64_t*>(smem);              // [65][65]
-    int64_t* zq = reinterpret_cast<int64_t*>(binom + 65 * 65);       // [n][D]
-    double* stage = reinterpret_cast<double*>(zq + (size_t)n * D);   // [kWarps][32][33]
-    for (int i = threadIdx.x; i < 65 * 65; i += blockDim.x) binom[i] = frr_binom(i / 65, i % 65);
+    const int nb = n + 1;                                             // binomial rows/cols 0..n
+    uint64_t* binom = reinterpret_cast<uint64_t*>(smem);              // [n+1][n+1]
+    int64_t* zq = reinterpret_cast<int64_t*>(binom + nb * nb);       // [n][D]
+    double* stage = reinterpret_cast<double*>(zq + (size_t)n * D);   // [kWarps][32][kRun + 1]
+    for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) binom[i] = frr_binom(i / nb, i % nb);
     for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
         int e = i / D, j = i % D;
         zq[i] = j < d ? bal.zq[(size_t)e * d + j] : 0;
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* st = stage + (size_t)warp * 32 * 33;
+    double* st = stage + (size_t)warp * 32 * (kRun + 1);
     const uint64_t fullmask = n == 64 ? ~0ull : ((1ull << n) - 1ull);
     const int64_t per_warp = 32 * kRun;
     for (int64_t wb = ((int64_t)blockIdx.x * kWarps + warp) * per_warp; wb < count;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uin
             int x = 0;
             for (int i = 0; i < t; i++) {
                 for (;;) {
-                    uint64_t cnk = binom[(n - x - 1) * 65 + (t - i - 1)];
+                    uint64_t cnk = binom[(n - x - 1) * nb + (t - i - 1)];
                     if (rank < cnk) break;
                     rank -= cnk;
                     x++;
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uin
                 mm &= mm - 1;
             }
             for (int r = 0; r < nrun; r++) {
-                st[lane * 33 + r] = small_stat<D>(S, d, bal.g, bal.cc, bal.cst);
+                st[lane * (kRun + 1) + r] = small_stat<D>(S, d, bal.g, bal.cc, bal.cst);
                 if (r + 1 < nrun) {
                     uint64_t xc = ~m & fullmask;
                     uint64_t cbit = xc & (0ull - xc);
@@ -361,9 +365,9 @@ __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uin
             }
         }
         __syncwarp();
-        for (int k = 0; k < 32; k++) {
+        for (int k = 0; k < kRun; k++) {  // coalesced: the warp's 32 * kRun statistics in rank order
             int64_t idx = wb + (int64_t)k * 32 + lane;
-            if (idx < count) out[idx] = st[(k * 32 + lane) / kRun * 33 + (k * 32 + lane) % kRun];
+            if (idx < count) out[idx] = st[(k * 32 + lane) / kRun * (kRun + 1) + (k * 32 + lane) % kRun];
         }
         __syncwarp();
     }
@@ -632,8 +636,8 @@ int launch_stats(const frr_balance_t* bal, uint64_t seed, const uint64_t* ids, c
 
 template <int D>
 int launch_exact_small(const frr_balance_t* bal, uint64_t rank_lo, int64_t count, double* out, void* stream) {
-    size_t smem = 65 * 65 * sizeof(uint64_t) + (size_t)bal->n * D * sizeof(int64_t) +
-                  (size_t)kWarps * 32 * 33 * sizeof(double);
+    size_t smem = (size_t)(bal->n + 1) * (bal->n + 1) * sizeof(uint64_t) + (size_t)bal->n * D * sizeof(int64_t) +
+                  (size_t)kWarps * 32 * (kRun + 1) * sizeof(double);
     auto kern = k_exact_small<D>;
     int rc = frr_prepare_kernel(kern, smem);
     if (rc) return rc;
