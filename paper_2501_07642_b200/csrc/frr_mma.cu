@@ -296,22 +296,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             TW(3, mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1));
             tc_fence_after();
             const uint32_t tl = tmem_base + ((uint32_t)((warp - c_w_tile0) * 32) << 16);
-            double racc[8], tq[8];
+            // d <= 128 here: one leaf of numpy's pairwise sum -- 8 accumulators
+            // over the full groups, their tree, then the tail added in order
+            double racc[8];
 #pragma unroll
-            for (int k = 0; k < 8; k++) racc[k] = tq[k] = 0.0;
+            for (int k = 0; k < 8; k++) racc[k] = 0.0;
+            double res = -0.0;
             for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
+                if (jb >= d) break;
                 int64_t Sj[8];
                 tc_limbs8(tl + (uint32_t)jb, S.L, S.dpad, pair32, Sj);
+                if (jb < full) {
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int j = jb + u;
-                    if (j < d) {
-                        double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), bal.cc[j]);
-                        double q = __dmul_rn(delta, delta);
-                        if (j < full) {
-                            racc[u] = j < 8 ? q : __dadd_rn(racc[u], q);
-                        } else {
-                            tq[u] = q;
+                    for (int u = 0; u < 8; u++) {
+                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), bal.cc[jb + u]);
+                        const double q = __dmul_rn(delta, delta);
+                        racc[u] = jb == 0 ? q : __dadd_rn(racc[u], q);
+                    }
+                } else {  // the tail group (full < d)
+                    if (d >= 8)
+                        res = __dadd_rn(__dadd_rn(__dadd_rn(racc[0], racc[1]), __dadd_rn(racc[2], racc[3])),
+                                        __dadd_rn(__dadd_rn(racc[4], racc[5]), __dadd_rn(racc[6], racc[7])));
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (jb + u < d) {
+                            const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), bal.cc[jb + u]);
+                            res = __dadd_rn(res, __dmul_rn(delta, delta));
                         }
                     }
                 }
@@ -319,17 +329,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars[BAR_TMEM_EMPTY]);
-            double res;
-            const int tail = d - full;
-            if (d < 8) {
-                res = -0.0;
-            } else {
+            if (d >= 8 && full == d)
                 res = __dadd_rn(__dadd_rn(__dadd_rn(racc[0], racc[1]), __dadd_rn(racc[2], racc[3])),
                                 __dadd_rn(__dadd_rn(racc[4], racc[5]), __dadd_rn(racc[6], racc[7])));
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++)
-                if (u < tail) res = __dadd_rn(res, tq[u]);
             const int64_t c = tile * BM + r;
             if (c < count) out[c] = __dmul_rn(__dadd_rn(0.0, res), cst);
         }
