@@ -70,6 +70,14 @@ class ClockSampler:
                  "-lms", os.environ.get("FRR_CLOCK_MS", "200")], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        # let nvidia-smi finish its NVML start-up (which can stall the GPU for
+        # milliseconds) before the timed region: wait for its first sample
+        deadline = time.time() + 3.0
+        while self.proc is not None and time.time() < deadline:
+            self.log.flush()
+            if os.fstat(self.log.fileno()).st_size > 0:
+                break
+            time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
