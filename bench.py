@@ -64,6 +64,9 @@ class ClockSampler:
         import tempfile
 
         self.log = tempfile.TemporaryFile(mode="w+")
+        if os.environ.get("FRR_NO_CLOCKS"):  # diagnostics only
+            self.proc = None
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -216,13 +219,19 @@ def run_ours(args):
     ops = DeviceSelectOps()
     stream = torch.cuda.current_stream()
 
+    host_marks = []
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         G.mc_stats_device(kern, design, lo, hi - lo, out=stats)
         if ev:
             ev[1].record(stream)
-        return select_k_smallest(stats, lo, k, ops, comm)
+            host_marks.append(time.perf_counter())
+        r = select_k_smallest(stats, lo, k, ops, comm)
+        if ev:
+            host_marks.append(time.perf_counter())
+        return r
 
     for _ in range(args.warmup):
         step()
@@ -231,12 +240,27 @@ def run_ours(args):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    # no interpreter garbage collection inside the timed region (as timeit
+    # does): a collection pass stalls the host between the select's kernels
+    import gc
+
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         t_start.record(stream)
+        marks[0].record(stream)
         for i in range(args.steps):
             res = step(evs[i])
+            marks[i + 1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
+    if os.environ.get("FRR_BENCH_DEBUG"):
+        print("steps ms:", [round(marks[i].elapsed_time(marks[i + 1]), 2) for i in range(args.steps)],
+              "pass1 ms:", [round(a.elapsed_time(b), 2) for a, b in evs],
+              "host select ms:", [round(1e3 * (host_marks[2 * i + 1] - host_marks[2 * i]), 1) for i in range(args.steps)],
+              file=sys.stderr)
     _barrier(world)
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end) / args.steps
