@@ -92,6 +92,9 @@ __device__ inline void frr_fill_steps(StepC* steps, int n, int t) {
 // Table entries per candidate: n uint16 entries padded to a multiple of 32
 // (whole 64-byte words for the packers); padding entries read as control.
 __host__ __device__ __forceinline__ int frr_table_len(int n) { return (n + 31) & ~31; }
+// Readable bytes every layout keeps after the last table (frr_warp_fy's
+// unpredicated re-read of padding steps reaches up to 63 entries past it).
+#define FRR_TABLE_SLACK 128
 
 __device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, int lane) {
     uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
@@ -163,8 +166,10 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         // store (self-swaps change nothing), then re-read: a higher lane's
         // store can be overwritten by a lower lane's in the same instruction,
         // so retry until the largest k holds (values at a position only grow,
-        // so "pending" is recomputed from a fresh read each time; r = k may
-        // lie past the table when d = 0, hence the d != 0 predicate)
+        // so "pending" is recomputed from a fresh read each time).  The
+        // re-read is unpredicated: with d = 0, r = k can lie up to 63 entries
+        // past the table (padding steps), which every layout leaves readable
+        // (FRR_TABLE_SLACK); the value is ignored there.
 #if FRR_FY_ROUNDS == 2
         const uint32_t lwa = (uint32_t)__cvta_generic_to_shared(lw);
         uint32_t any;
@@ -175,10 +180,10 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
             "@q0 st.shared.u16 [%2], %3;\n\t"
             "@q1 st.shared.u16 [%5], %6;\n\t"
             "bar.warp.sync 0xffffffff;\n\t"
-            "@q0 ld.shared.u16 x0, [%2];\n\t"
-            "@q1 ld.shared.u16 x1, [%5];\n\t"
-            "@q0 setp.lt.u32 q0, x0, %3;\n\t"
-            "@q1 setp.lt.u32 q1, x1, %6;\n\t"
+            "ld.shared.u16 x0, [%2];\n\t"
+            "ld.shared.u16 x1, [%5];\n\t"
+            "setp.lt.and.u32 q0, x0, %3, q0;\n\t"
+            "setp.lt.and.u32 q1, x1, %6, q1;\n\t"
             "or.pred q0, q0, q1;\n\t"
             "vote.sync.any.pred q0, q0, 0xffffffff;\n\t"
             "selp.u32 %0, 1, 0, q0;\n\t}"
@@ -240,16 +245,23 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(lw);
         const uint32_t ea = base + 2u * (uint32_t)n, vbase = base - 2u;
         uint32_t pa = base + 2u * (uint32_t)(t + lane), qa = pa;
-        while (pa < ea) {
-            uint32_t v;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(qa) : "memory");
-            if (v == 0) {
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(FRR_CTL) : "memory");
-                pa += 64u;
-                qa = pa;
-            } else {
-                qa = vbase + 2u * v;
-            }
+        if (pa < ea) {
+            // one link per iteration: a zero entry is a root (mark it, move to
+            // this lane's next start), else follow to lw[v - 1]
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t.reg .u32 v, nx;\n"
+                "FRR_WALK_LOOP:\n\t"
+                "ld.shared.u16 v, [%0];\n\t"
+                "setp.eq.u32 p, v, 0;\n\t"
+                "mad.lo.u32 nx, v, 2, %3;\n\t"
+                "@p st.shared.u16 [%0], %4;\n\t"
+                "@p add.u32 %1, %1, 64;\n\t"
+                "selp.u32 %0, %1, nx, p;\n\t"
+                "setp.lt.u32 q, %1, %2;\n\t"
+                "@q bra FRR_WALK_LOOP;\n\t}"
+                : "+r"(qa), "+r"(pa)
+                : "r"(ea), "r"(vbase), "r"((uint32_t)n | FRR_CTL)  // low half FRR_CTL, kept in a register
+                : "memory");
         }
     }
     __syncwarp();

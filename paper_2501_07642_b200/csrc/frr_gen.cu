@@ -39,7 +39,7 @@ WarpPlan plan_warps(int t, bool needs_steps, size_t fixed, size_t per_warp) {
     for (int g = 0; g < 2; g++) {
         const bool gsteps = g == 1;
         if (gsteps && !needs_steps) break;
-        const size_t f = fixed + (gsteps ? 0 : steps_b);
+        const size_t f = fixed + FRR_TABLE_SLACK + (gsteps ? 0 : steps_b);
         for (int w = 1; w <= kPlanWarps; w++) {
             const size_t smem = f + (size_t)w * per_warp;
             if (smem > cap) break;

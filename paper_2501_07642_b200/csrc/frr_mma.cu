@@ -104,7 +104,7 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     o += (size_t)s.nfy * frr_table_len(s.n) * 2;
     o = align_up(o, 16);
     p.bars = o;
-    o += 32 * 8 + 16;
+    o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
     p.total = o + 1024;  // slack for base alignment
     return p;
 }

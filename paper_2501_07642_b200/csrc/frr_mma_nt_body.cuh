@@ -102,7 +102,7 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     o += MAX_LEAVES;
     o = up(o, 16);
     p.bars = o;
-    o += 32 * 8 + 16;
+    o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
     p.total = o + 1024;
     return p;
 }
