@@ -63,20 +63,20 @@ __host__ __device__ __forceinline__ StepC frr_make_step(int n, int k) {
     return s;
 }
 
-__device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s) {
+__device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s, uint32_t zero = 0u, uint32_t zero2 = 0u) {
     // written on 32-bit halves so the result stays a plain 32-bit register
     const uint32_t ulo = (uint32_t)u, uhi = (uint32_t)(u >> 32);
     const uint32_t mlo = (uint32_t)s.M, mhi = (uint32_t)(s.M >> 32);
     uint32_t ylo, yhi;  // y = uhi * c2 + ulo  (< 2^48)
-    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo));
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo), "r"(zero));
     // low = M * y mod 2^64
     const uint32_t llo = mlo * ylo;
     const uint32_t lhi = __umulhi(mlo, ylo) + mhi * ylo + mlo * yhi;
     // result = floor(low * b / 2^64) = hi32(lhi * b + umulhi(llo, b))
     uint32_t rhi;  // the low word of the sum only feeds the carry
-    asm("{\n\t.reg .u32 rlo;\n\tmad.lo.cc.u32 rlo, %1, %2, %3;\n\tmadc.hi.u32 %0, %1, %2, 0;\n\t}"
+    asm("{\n\t.reg .u32 rlo;\n\tmad.lo.cc.u32 rlo, %1, %2, %3;\n\tmadc.hi.u32 %0, %1, %2, %4;\n\t}"
         : "=r"(rhi)
-        : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)));
+        : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)), "r"(zero2));
     return rhi;
 }
 
@@ -93,8 +93,8 @@ __device__ inline void frr_fill_steps(StepC* steps, int n, int t) {
 // (whole 64-byte words for the packers); padding entries read as control.
 __host__ __device__ __forceinline__ int frr_table_len(int n) { return (n + 31) & ~31; }
 // Readable bytes every layout keeps after the last table (frr_warp_fy's
-// unpredicated re-read of padding steps reaches up to 63 entries past it).
-#define FRR_TABLE_SLACK 128
+// unpredicated re-read of padding steps reaches up to 127 entries past it).
+#define FRR_TABLE_SLACK 256
 
 __device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, int lane) {
     uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
@@ -117,7 +117,8 @@ __device__ __forceinline__ void frr_table_fill(uint16_t* lw, int n, uint16_t v, 
 // table: lw[p] = 1 + (last step k < p with r_k = p).  The final content of a
 // position p >= t is found by following lw links to a never-written position
 // (its original element); those t..n-1 contents are the control units.
-__device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uint32_t& hmax) {
+__device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uint32_t& hmax, uint32_t zero = 0u,
+                                                uint32_t zero2 = 0u) {
     const uint4 q = *reinterpret_cast<const uint4*>(sp);  // one LDS.128
     StepC s;
     s.b = q.x;
@@ -125,11 +126,11 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
     s.M = ((uint64_t)q.w << 32) | q.z;
     const uint64_t u = frr_mix64(x);
     hmax = max(hmax, (uint32_t)(u >> 32));  // a rejection needs hi(u) == 0xFFFFFFFF
-    return frr_mod_step(u, s);
+    return frr_mod_step(u, s, zero, zero2);
 }
 
 #ifndef FRR_FY_ROUNDS
-#define FRR_FY_ROUNDS 2
+#define FRR_FY_ROUNDS 4
 #endif
 
 __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
@@ -153,25 +154,30 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
     const uint64_t stride = 32ull * R * FRR_GOLDEN;
     // (padding steps k >= t have b = 1: d = 0, no store; a spurious flag from
     // them (p ~ 2^-32) only triggers the exact slow path)
-    for (int base = 0; base < t; base += 32 * R) {
-        uint32_t d[R], r[R], v[R];
-#pragma unroll
-        for (int i = 0; i < R; i++) {
-            const int k = base + 32 * i + sl;
-            d[i] = frr_fy_draw(x[i], steps + k, hmax);
-            r[i] = (uint32_t)k + d[i];
-            v[i] = (uint32_t)k + 1;
-            x[i] += stride;
-        }
-        // store (self-swaps change nothing), then re-read: a higher lane's
-        // store can be overwritten by a lower lane's in the same instruction,
-        // so retry until the largest k holds (values at a position only grow,
-        // so "pending" is recomputed from a fresh read each time).  The
-        // re-read is unpredicated: with d = 0, r = k can lie up to 63 entries
-        // past the table (padding steps), which every layout leaves readable
-        // (FRR_TABLE_SLACK); the value is ignored there.
+    //
+    // Each round stores, then re-reads: a higher lane's store can be
+    // overwritten by a lower lane's in the same instruction, so retry until
+    // the largest k holds (values at a position only grow, so "pending" is
+    // recomputed from a fresh read each time).
 #if FRR_FY_ROUNDS == 2
-        const uint32_t lwa = (uint32_t)__cvta_generic_to_shared(lw);
+    // loop-carried step pointer, table address of lw[k] and k + 1 (round 0;
+    // round 1 is +32 steps) instead of per-iteration index arithmetic.  The
+    // re-read is unpredicated: with d = 0, r = k can lie up to 63 entries
+    // past the table (padding steps), which every layout leaves readable
+    // (FRR_TABLE_SLACK); the value is ignored there.
+    const uint32_t lwa = (uint32_t)__cvta_generic_to_shared(lw);
+    const StepC* sp = steps + sl;
+    uint32_t ka = lwa + 2u * (uint32_t)sl, v0 = (uint32_t)sl + 1u;
+    const uint32_t kend = ka + 2u * (uint32_t)t;  // base < t
+    // zeros opaque to the compiler: live zero high words of the 64-bit
+    // addends in frr_mod_step (saves re-zeroing a register pair per use)
+    uint32_t z[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) z[i] = (uint32_t)(t + i) >> 31;
+    for (; ka < kend; ka += 128u, v0 += 64u, sp += 64) {
+        const uint32_t d0 = frr_fy_draw(x[0], sp, hmax, z[0], z[1]), d1 = frr_fy_draw(x[1], sp + 32, hmax, z[2], z[3]);
+        x[0] += stride;
+        x[1] += stride;
         uint32_t any;
         asm volatile(
             "{\n\t.reg .pred q0, q1;\n\t.reg .u32 x0, x1;\n\t"
@@ -188,10 +194,69 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
             "vote.sync.any.pred q0, q0, 0xffffffff;\n\t"
             "selp.u32 %0, 1, 0, q0;\n\t}"
             : "=r"(any)
-            : "r"(d[0]), "r"(lwa + 2u * r[0]), "r"(v[0]), "r"(d[1]), "r"(lwa + 2u * r[1]), "r"(v[1])
+            : "r"(d0), "r"(ka + 2u * d0), "r"(v0), "r"(d1), "r"(ka + 64u + 2u * d1), "r"(v0 + 32u)
             : "memory");
         if (any) {
+            const uint32_t d[2] = {d0, d1}, v[2] = {v0, v0 + 32u}, r[2] = {v0 - 1u + d0, v0 + 31u + d1};
+#elif FRR_FY_ROUNDS == 4
+    const uint32_t lwa = (uint32_t)__cvta_generic_to_shared(lw);
+    const StepC* sp = steps + sl;
+    uint32_t ka = lwa + 2u * (uint32_t)sl, v0 = (uint32_t)sl + 1u;
+    const uint32_t kend = ka + 2u * (uint32_t)t;
+    uint32_t z[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) z[i] = (uint32_t)(t + i) >> 31;
+    for (; ka < kend; ka += 256u, v0 += 128u, sp += 128) {
+        uint32_t d[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            d[i] = frr_fy_draw(x[i], sp + 32 * i, hmax, z[(2 * i) & 3], z[(2 * i + 1) & 3]);
+            x[i] += stride;
+        }
+        uint32_t any;
+        asm volatile(
+            "{\n\t.reg .pred q0, q1, q2, q3;\n\t.reg .u32 x0, x1, x2, x3;\n\t"
+            "setp.ne.u32 q0, %1, 0;\n\t"
+            "setp.ne.u32 q1, %4, 0;\n\t"
+            "setp.ne.u32 q2, %7, 0;\n\t"
+            "setp.ne.u32 q3, %10, 0;\n\t"
+            "@q0 st.shared.u16 [%2], %3;\n\t"
+            "@q1 st.shared.u16 [%5], %6;\n\t"
+            "@q2 st.shared.u16 [%8], %9;\n\t"
+            "@q3 st.shared.u16 [%11], %12;\n\t"
+            "bar.warp.sync 0xffffffff;\n\t"
+            "ld.shared.u16 x0, [%2];\n\t"
+            "ld.shared.u16 x1, [%5];\n\t"
+            "ld.shared.u16 x2, [%8];\n\t"
+            "ld.shared.u16 x3, [%11];\n\t"
+            "setp.lt.and.u32 q0, x0, %3, q0;\n\t"
+            "setp.lt.and.u32 q1, x1, %6, q1;\n\t"
+            "setp.lt.and.u32 q2, x2, %9, q2;\n\t"
+            "setp.lt.and.u32 q3, x3, %12, q3;\n\t"
+            "or.pred q0, q0, q1;\n\t"
+            "or.pred q2, q2, q3;\n\t"
+            "or.pred q0, q0, q2;\n\t"
+            "vote.sync.any.pred q0, q0, 0xffffffff;\n\t"
+            "selp.u32 %0, 1, 0, q0;\n\t}"
+            : "=r"(any)
+            : "r"(d[0]), "r"(ka + 2u * d[0]), "r"(v0), "r"(d[1]), "r"(ka + 64u + 2u * d[1]), "r"(v0 + 32u),
+              "r"(d[2]), "r"(ka + 128u + 2u * d[2]), "r"(v0 + 64u), "r"(d[3]), "r"(ka + 192u + 2u * d[3]),
+              "r"(v0 + 96u)
+            : "memory");
+        if (any) {
+            const uint32_t v[4] = {v0, v0 + 32u, v0 + 64u, v0 + 96u};
+            const uint32_t r[4] = {v[0] - 1u + d[0], v[1] - 1u + d[1], v[2] - 1u + d[2], v[3] - 1u + d[3]};
 #else
+    for (int base = 0; base < t; base += 32 * R) {
+        uint32_t d[R], r[R], v[R];
+#pragma unroll
+        for (int i = 0; i < R; i++) {
+            const int k = base + 32 * i + sl;
+            d[i] = frr_fy_draw(x[i], steps + k, hmax);
+            r[i] = (uint32_t)k + d[i];
+            v[i] = (uint32_t)k + 1;
+            x[i] += stride;
+        }
 #pragma unroll
         for (int i = 0; i < R; i++)
             if (d[i] != 0) lw[r[i]] = (uint16_t)v[i];

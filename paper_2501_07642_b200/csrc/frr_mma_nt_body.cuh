@@ -103,6 +103,7 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     o = up(o, 16);
     p.bars = o;
     o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
+    static_assert(32 * 8 + 16 >= FRR_TABLE_SLACK, "table slack");
     p.total = o + 1024;
     return p;
 }

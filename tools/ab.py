@@ -43,6 +43,9 @@ for p in libs:
     f.restype = ctypes.c_int
     f.argtypes = [ctypes.POINTER(N.Balance), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                   ctypes.c_void_p]
+    L.frr_last_error.restype = ctypes.c_char_p
+    f.last_error = L.frr_last_error
+    f.lib = p
     handles.append(f)
 
 
@@ -50,7 +53,7 @@ def launch(f):
     rc = f(ctypes.byref(s), design.root_seed, 0, M, ctypes.c_void_p(out.data_ptr()),
            ctypes.c_void_p(stream.cuda_stream))
     if rc:
-        raise RuntimeError(f"rc={rc}")
+        raise RuntimeError(f"{f.lib}: rc={rc}: {f.last_error().decode()}")
 
 
 bad = []

@@ -55,3 +55,9 @@ if M:
     print(f"warp-instructions per candidate: {tot_i / M:.1f}")
     for c, k in sorted(cls.items(), key=lambda x: -x[0] * x[1])[:12]:
         print(f"  {c:>12} x {k:>4} = {c * k / M:8.1f} per candidate")
+    if len(sys.argv) > 3:
+        # the hottest SASS lines (executions per candidate) with their text
+        rows = sorted(src[2:], key=lambda r: -int(r[ix["Instructions Executed"]] or 0))[: int(sys.argv[3])]
+        for r in rows:
+            c = int(r[ix["Instructions Executed"]] or 0)
+            print(f"  {c / M:8.2f}  {r[ix['Address']]:>6s}  {r[ix['Source']][:80]}")
