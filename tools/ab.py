@@ -62,6 +62,14 @@ for f in handles:
     launch(f)
     torch.cuda.synchronize()
     bad.append(int((out.cpu().numpy().view(np.uint64) != want.view(np.uint64)).sum()))
+# warm-up: the first ~1-2 s of back-to-back tensor-heavy launches on a fresh
+# box are erratic (power ramp); launch the first build until AB_WARM seconds pass
+import time  # noqa: E402
+
+t_warm = time.time() + float(os.environ.get("AB_WARM", "2"))
+while time.time() < t_warm:
+    launch(handles[0])
+    torch.cuda.synchronize()
 times = [[] for _ in handles]
 for _ in range(R):
     for i, f in enumerate(handles):
