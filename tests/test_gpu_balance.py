@@ -76,7 +76,9 @@ MC_CASES = [(16, 20, 8, "ridge"), (17, 24, 8, "ridge"), (64, 33, 30, "exact"), (
             # single-pass kernel at large n: fewer generator warps / one bit buffer
             (5000, 64, 2500, "exact"), (3000, 40, 1500, "exact"), (12000, 24, 6000, "exact"),
             # N-tiled kernel at large n: one bit buffer, fewer generators
-            (5000, 128, 2500, "exact")]
+            (5000, 128, 2500, "exact"),
+            # t = n - 1 with n a multiple of 32: padding steps re-read past the table
+            (1056, 64, 1055, "exact"), (1056, 8, 1055, "exact"), (1056, 40, 1055, "ridge")]
 
 
 @pytest.mark.parametrize("n,d,t,mode", MC_CASES)

@@ -99,6 +99,20 @@ def test_large_keys_pool_vs_oracle():
     assert got.tolist() == want
 
 
+def test_keys_pool_t_near_n_vs_oracle():
+    """k_dim with t = n - 1, n a multiple of 32 (padding steps re-read past the table)."""
+    n, t, m = 1056, 1055, 3000
+    keys = np.column_stack([np.full(m, 9, dtype=np.uint64), 13 * np.arange(m, dtype=np.uint64)])
+    pool = frr.RandomizationPool(
+        design=frr.DesignSpec(n, t, accept_prob=1.0, max_draws=m * 13, batch_size=13, root_seed=9),
+        stats=np.zeros(m), threshold_value=0.0, n_candidates=m * 13, accepted_indices=13 * np.arange(m), keys=keys)
+    W = frr.regenerate_assignments(pool)
+    assert np.array_equal(W, O.c_batch_assign(9, 13 * np.arange(m, dtype=np.uint64), n, t))
+    y = np.random.default_rng(56).standard_normal(n) + W[0]
+    res = frr.randomization_pvalue(W[0], y, pool)
+    assert np.array_equal(res.stat_distribution, O.c_dim_rows(W, y, t))
+
+
 def test_label_symmetry_and_constant_y(pool8):
     rows = pool8.assignments
     y = np.random.default_rng(204).standard_normal(8)
