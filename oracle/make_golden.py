@@ -214,14 +214,64 @@ def gen_sim():
     np.savez_compressed(os.path.join(OUT, "sim.npz"), **out)
 
 
+def _unmix64(z: int) -> int:
+    """Inverse of keys.py:107-115 (xorshifts and odd multipliers are bijections)."""
+    def unxorshift(y, s):
+        x = y
+        for _ in range(64 // s + 1):
+            x = y ^ (x >> s)
+        return x & M64
+    z = unxorshift(z, 31)
+    z = (z * pow(0x94D049BB133111EB, -1, 1 << 64)) & M64
+    z = unxorshift(z, 27)
+    z = (z * pow(0xBF58476D1CE4E5B9, -1, 1 << 64)) & M64
+    return unxorshift(z, 30)
+
+
+def crafted_seed(draw: int, step: int, u: int) -> int:
+    """A root seed whose key (seed, draw) has stream output `u` at Fisher-Yates
+    step `step` (no earlier rejection): state0 = s_step - (step+1) C with
+    s_step = mix64^-1(u); seed = (mix64^-1(state0) - C) ^ (draw C)."""
+    g = rk.GOLDEN
+    s_step = _unmix64(u)
+    state0 = (s_step - (step + 1) * g) & M64
+    pre = _unmix64(state0)
+    seed = ((pre - g) & M64) ^ ((draw * g) & M64)
+    assert rk.derive_state(rk.AssignmentKey(seed, draw)) == state0
+    assert rk.mix64((state0 + (step + 1) * g) & M64) == u
+    return seed
+
+
+def gen_rejection():
+    """Keys whose stream hits the rejection zone of _bounded (keys.py:148-155)
+    at a chosen step (u = 2^64 - 1: rejected for every non-power-of-two
+    bound), or only sets the GPU's "hi(u) == 0xFFFFFFFF" flag without a
+    rejection (u = 0xFFFFFFFF00000000); outputs from the reference."""
+    draw = 12345
+    cases = [  # (n, t, step, u)
+        (1000, 500, 7, M64), (1000, 500, 0, M64), (1000, 500, 499, M64), (1000, 500, 300, 0xFFFFFFFF00000000),
+        (20, 10, 3, M64), (5000, 2500, 2000, M64), (2000, 1000, 999, M64), (1056, 1055, 1000, M64),
+        (34, 17, 16, M64)]
+    out = {"cases": np.array([c[:3] for c in cases], dtype=np.int64), "draw": np.array(draw, dtype=np.uint64)}
+    seeds = []
+    for i, (n, t, step, u) in enumerate(cases):
+        seed = crafted_seed(draw, step, u)
+        seeds.append(seed)
+        W = rk.batch_assignments(seed, np.array([draw, draw + 1, 0], dtype=np.uint64), n, t)
+        assert np.array_equal(W[0], np.asarray(rk.assignment_from_key(rk.AssignmentKey(seed, draw), n, t).bits))
+        out[f"bits_{i}"] = np.packbits(W.astype(np.uint8), axis=1, bitorder="little")
+    out["seeds"] = np.array(seeds, dtype=np.uint64)
+    np.savez_compressed(os.path.join(OUT, "rejection.npz"), **out)
+
+
+GENERATORS = {"pairwise": lambda: gen_pairwise(), "keys": lambda: gen_keys(), "balance": lambda: gen_balance(),
+              "pools": lambda: gen_pools(), "inference": lambda: gen_inference(), "sim": lambda: gen_sim(),
+              "rejection": lambda: gen_rejection()}
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     print("reference fastrr", fastrr.__version__, "from", REF)
-    gen_pairwise()
-    gen_keys()
-    gen_balance()
-    gen_pools()
-    gen_inference()
-    gen_sim()
+    for name in sys.argv[1:] or list(GENERATORS):
+        GENERATORS[name]()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -174,3 +174,22 @@ def test_integration_md_ctypes_stub():
     assert rc == 0, lib.frr_last_error()
     want = G.mc_stats_device(kernel, design, 0, design.max_draws).cpu().numpy()
     assert bits_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("case,d,path", [(0, 64, "auto"), (0, 64, "cuda_core"), (2, 8, "auto"), (3, 40, "auto"),
+                                         (6, 100, "auto"), (7, 64, "auto"), (5, 24, "auto")])
+def test_mc_stats_rejection_keys(golden, case, d, path, monkeypatch):
+    """Pass-1 statistics of a draw range containing a key crafted to hit the
+    rejection zone (tests/golden/rejection.npz) on every pass-1 kernel."""
+    g = golden("rejection")
+    n, t, _ = (int(v) for v in g["cases"][case])
+    seed, draw = int(g["seeds"][case]), int(g["draw"])
+    X = np.random.default_rng(n + d).standard_normal((n, d))
+    monkeypatch.setenv("FRR_MC_PATH", path)
+    kern = frr.precompute_precision(X, "ridge")._kernel
+    design = frr.DesignSpec(n, t, accept_prob=1.0, max_draws=10**6, batch_size=1, root_seed=seed,
+                            precision_mode="ridge")
+    lo, M = draw - 200, 400
+    st = G.mc_stats_device(kern, design, lo, M).cpu().numpy()
+    bal = O.Balance(kern._zq, kern._inv_scale_sq)
+    assert bits_equal(st, O.c_mc_stats(bal, t, seed, lo, M))

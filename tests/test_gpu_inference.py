@@ -113,6 +113,25 @@ def test_keys_pool_t_near_n_vs_oracle():
     assert np.array_equal(res.stat_distribution, O.c_dim_rows(W, y, t))
 
 
+def test_keys_pool_with_rejection_key(golden):
+    """Regeneration + test statistics for a keys pool containing a key
+    crafted to hit the rejection zone (tests/golden/rejection.npz, n=5000)."""
+    g = golden("rejection")
+    n, t, _ = (int(v) for v in g["cases"][5])
+    seed, draw = int(g["seeds"][5]), int(g["draw"])
+    ids = np.arange(draw - 50, draw + 50, dtype=np.uint64)
+    keys = np.column_stack([np.full(ids.size, seed, dtype=np.uint64), ids])
+    pool = frr.RandomizationPool(
+        design=frr.DesignSpec(n, t, accept_prob=1.0, max_draws=draw + 50, batch_size=1, root_seed=seed),
+        stats=np.zeros(ids.size), threshold_value=0.0, n_candidates=draw + 50,
+        accepted_indices=ids.astype(np.int64), keys=keys)
+    W = frr.regenerate_assignments(pool)
+    assert np.array_equal(W, O.c_batch_assign(seed, ids, n, t))
+    y = np.random.default_rng(57).standard_normal(n) + W[50]
+    res = frr.randomization_pvalue(W[50], y, pool)
+    assert np.array_equal(res.stat_distribution, O.c_dim_rows(W, y, t))
+
+
 def test_label_symmetry_and_constant_y(pool8):
     rows = pool8.assignments
     y = np.random.default_rng(204).standard_normal(8)

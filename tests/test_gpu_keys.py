@@ -81,3 +81,18 @@ def test_invalid(n, t):
         frr.batch_assignments(0, np.arange(3, dtype=np.uint64), n, t)
     with pytest.raises(InvalidDesignError):
         frr.batch_assignments(5, np.array([-1]), 6, 3)
+
+
+REJ_CASES = range(9)
+
+
+@pytest.mark.parametrize("case", REJ_CASES)
+def test_rejection_keys_golden(golden, case):
+    """The GPU generator's exact sequential path (taken when a stream output
+    has hi(u) == 0xFFFFFFFF) against the reference, for keys crafted to be
+    rejected at a chosen step (first, middle, last) or only flagged."""
+    g = golden("rejection")
+    n, t, _ = (int(v) for v in g["cases"][case])
+    seed, draw = int(g["seeds"][case]), int(g["draw"])
+    draws = np.array([draw, draw + 1, 0], dtype=np.uint64)
+    assert np.array_equal(frr.batch_assignments(seed, draws, n, t), unpack(g[f"bits_{case}"], n))
