@@ -401,6 +401,52 @@ __device__ void plan_build(PwPlan& P, int off, int len) {
 
 __host__ __device__ inline int plan_max_leaves(int n) { return n / 64 + 2; }
 
+// The leaf-combination tree of numpy's pairwise sum as parallel rounds: node
+// (L, R) adds its right child's value into its left child's slot (a node's
+// slot is its leftmost leaf).  Nodes in one round touch disjoint slots and
+// only read values finished in earlier rounds, so a warp evaluates the tree
+// round by round instead of one lane walking the postfix program.
+// sched[2e], sched[2e+1] = (L, R) of entry e; round r holds entries
+// [round_start[r], round_start[r+1]).  Scratch: 3 * nleaf ints.  Returns the
+// number of rounds.
+constexpr int kMaxRounds = 32;
+__device__ int plan_rounds(const int16_t* tok, int ntok, int nleaf, int* scratch, int16_t* sched,
+                           int* round_start) {
+    int* stk_slot = scratch;
+    int* stk_h = scratch + nleaf;
+    int* ent_r = scratch + 2 * nleaf;  // round of entry e (postfix order), its (L, R) staged in sched
+    int sp = 0, ne = 0, nr = 0;
+    for (int i = 0; i < ntok; i++) {
+        if (tok[i] >= 0) {
+            stk_slot[sp] = tok[i];
+            stk_h[sp++] = 0;
+        } else {
+            sp--;
+            const int r = max(stk_h[sp - 1], stk_h[sp]);
+            ent_r[ne] = r;
+            sched[2 * ne] = (int16_t)stk_slot[sp - 1];
+            sched[2 * ne + 1] = (int16_t)stk_slot[sp];
+            ne++;
+            stk_h[sp - 1] = r + 1;
+            nr = max(nr, r + 1);
+        }
+    }
+    // stable counting sort of the entries by round, in place through scratch
+    for (int r = 0; r <= nr; r++) round_start[r] = 0;
+    for (int e = 0; e < ne; e++) round_start[ent_r[e] + 1]++;
+    for (int r = 0; r < nr; r++) round_start[r + 1] += round_start[r];
+    int* lr = stk_slot;  // (L, R) packed, reusing the stack area (2 * nleaf ints >= ne)
+    for (int e = 0; e < ne; e++) lr[e] = (int)sched[2 * e] | ((int)sched[2 * e + 1] << 16);
+    int* fill = stk_h;  // reused: per-round fill pointers (nr <= kMaxRounds)
+    for (int r = 0; r < nr; r++) fill[r] = round_start[r];
+    for (int e = 0; e < ne; e++) {
+        const int d = fill[ent_r[e]]++;
+        sched[2 * d] = (int16_t)(lr[e] & 0xFFFF);
+        sched[2 * d + 1] = (int16_t)(lr[e] >> 16);
+    }
+    return nr;
+}
+
 template <int SRC, bool GS>
 __global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows,
                                                   int64_t m, int n, int t, const double* __restrict__ y,
@@ -420,14 +466,19 @@ __global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint6
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + ((toff + 15) & ~(size_t)15));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint16_t* lw = tables + (size_t)warp * frr_table_len(n);
+    __shared__ int s_round[kMaxRounds + 1];
+    __shared__ int s_nround;
     if (threadIdx.x == 0) {
         PwPlan P{0, 0, leaf_off, leaf_len, tok};
         plan_build(P, 0, n);
         s_nleaf = P.nleaf;
         s_ntok = P.ntok;
+        // the round schedule overwrites tok (2 * (nleaf - 1) <= 2 * maxl
+        // entries); scratch: the first 3 * nleaf ints of leafres
+        s_nround = plan_rounds(tok, P.ntok, P.nleaf, reinterpret_cast<int*>(leafres), tok, s_round);
     }
     __syncthreads();
-    const int nleaf = s_nleaf, ntok = s_ntok;
+    const int nleaf = s_nleaf, nround = s_nround;
     double* rt = leafres + (size_t)warp * 2 * maxl;
     double* rc = rt + maxl;
     const int words = (n + 31) >> 5;
@@ -500,22 +551,17 @@ __global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint6
         }
         same = __all_sync(FRR_FULL, same);
         __syncwarp();
-        if (lane == 0) {
-            double stk_t[24], stk_c[24];
-            int sp = 0;
-            for (int i = 0; i < ntok; i++) {
-                int tk = tok[i];
-                if (tk >= 0) {
-                    stk_t[sp] = rt[tk];
-                    stk_c[sp] = rc[tk];
-                    sp++;
-                } else {
-                    sp--;
-                    stk_t[sp - 1] = __dadd_rn(stk_t[sp - 1], stk_t[sp]);
-                    stk_c[sp - 1] = __dadd_rn(stk_c[sp - 1], stk_c[sp]);
-                }
+        // the leaf-combination tree, one round of independent nodes at a time
+        for (int rd = 0; rd < nround; rd++) {
+            for (int e = s_round[rd] + lane; e < s_round[rd + 1]; e += 32) {
+                const int L = tok[2 * e], R = tok[2 * e + 1];
+                rt[L] = __dadd_rn(rt[L], rt[R]);
+                rc[L] = __dadd_rn(rc[L], rc[R]);
             }
-            double s_t = __dadd_rn(0.0, stk_t[0]), s_c = __dadd_rn(0.0, stk_c[0]);
+            __syncwarp();
+        }
+        if (lane == 0) {
+            double s_t = __dadd_rn(0.0, rt[0]), s_c = __dadd_rn(0.0, rc[0]);
             a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
             if (b) b[c] = __dsub_rn(__dmul_rn((double)pt, inv_t), __dmul_rn((double)pc, inv_c));
             if (match && same) atomicOr(match, 1);
