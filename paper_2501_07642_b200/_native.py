@@ -145,3 +145,47 @@ def check(rc: int, what: str):
 
 def call(name: str, *args):
     check(getattr(lib(), name)(*args), name)
+
+
+
+STAGE_MIN_BYTES = 1 << 20
+STAGE_MAX_BYTES = 1 << 31
+_stage_lock = threading.Lock()
+_stage = {"buf": None, "pool": None}
+
+
+def _stage_buffer(nbytes: int):
+    torch = torch_mod()
+    buf = _stage["buf"]
+    if buf is None or buf.numel() < nbytes:
+        size = 1 << max(24, (nbytes - 1).bit_length())
+        _stage["buf"] = buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+    return buf
+
+
+def to_host(t):
+    """Device tensor -> numpy array (a fresh, caller-owned array).  Large
+    results (accepted indices, statistics, assignment rows) go through one
+    reused page-locked staging buffer (one DMA at full rate) and a parallel
+    host copy: a pageable .cpu() of the 79 MB C4 row matrix runs at ~2 GB/s,
+    this path at ~16 GB/s, and no page-locked memory is handed to callers."""
+    torch = torch_mod()
+    nbytes = t.numel() * t.element_size()
+    if not t.is_cuda or nbytes < STAGE_MIN_BYTES or nbytes > STAGE_MAX_BYTES:
+        return t.cpu().numpy()
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    dst = out.reshape(-1).view(np.uint8)
+    with _stage_lock:
+        buf = _stage_buffer(nbytes)[:nbytes]
+        buf.copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        src = buf.numpy()
+        if _stage["pool"] is None:
+            _stage["pool"] = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)))
+        step = max(1 << 20, -(-nbytes // 8))
+        list(_stage["pool"].map(lambda a: np.copyto(dst[a:a + step], src[a:a + step]), range(0, nbytes, step)))
+    return out

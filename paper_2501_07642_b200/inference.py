@@ -189,7 +189,7 @@ def randomization_pvalue(obs_w, obs_y, pool: RandomizationPool, statistic=None) 
         in_pool = bool((mat == w).all(axis=1).any())
     else:
         ps = _PoolStats(pool, w, y)
-        dist = ps.a.cpu().numpy()
+        dist = N.to_host(ps.a)
         tau_obs = ps.tau_obs
         in_pool = ps.in_pool
     if not in_pool:
@@ -326,7 +326,7 @@ def randomization_test(obs_w=None, obs_y=None, pool: RandomizationPool | None = 
                           "the p-value may fall below 1/n_accepted", stacklevel=2)
         count = int(ps.counts([0.0], [abs(ps.tau_obs)])[0])
         res = TestResult(p_value=float(count) / ps.m, tau_obs=ps.tau_obs, fi=None,
-                         stat_distribution=ps.a.cpu().numpy(), alpha=None, obs_in_pool=ps.in_pool)
+                         stat_distribution=N.to_host(ps.a), alpha=None, obs_in_pool=ps.in_pool)
         if find_fi:
             res.fi = _fi_from_stats(ps, alpha)
             res.alpha = alpha

@@ -132,7 +132,7 @@ def batch_assignments(root_seed: int, draw_indices, n_units: int, n_treated: int
     if draws.shape[0] == 0:
         return np.zeros((0, n_units), dtype=np.int8)
     rows = regen_rows_device(root_seed, to_device_u64(draws), n_units, n_treated)
-    return rows.cpu().numpy()
+    return N.to_host(rows)
 
 
 def assignment_from_key(key: AssignmentKey, n_units: int, n_treated: int) -> Assignment:
