@@ -73,14 +73,18 @@ class ClockSampler:
                  "-lms", os.environ.get("FRR_CLOCK_MS", "200")], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
-        # let nvidia-smi finish its NVML start-up (which can stall the GPU for
-        # milliseconds) before the timed region: wait for its first sample
-        deadline = time.time() + 3.0
+        # let nvidia-smi finish its NVML start-up before the timed region:
+        # its first samples stall CUDA API calls of this process (measured:
+        # the timed step that overlapped the second sample took 12-100 ms
+        # longer), so wait until two samples are written
+        deadline = time.time() + 5.0
         while self.proc is not None and time.time() < deadline:
             self.log.flush()
-            if os.fstat(self.log.fileno()).st_size > 0:
+            self.log.seek(0)
+            if sum(1 for _ in self.log) >= 2:
                 break
             time.sleep(0.01)
+        self.log.seek(0, os.SEEK_END)
         return self
 
     def __exit__(self, *a):
@@ -220,6 +224,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     host_marks = []
+    step_traces = []
 
     def step(ev=None):
         if ev:
@@ -228,16 +233,16 @@ def run_ours(args):
         if ev:
             ev[1].record(stream)
             host_marks.append(time.perf_counter())
+            if os.environ.get("FRR_BENCH_DEBUG"):
+                import paper_2501_07642_b200._select as SEL
+
+                SEL.TRACE = []
+                step_traces.append(SEL.TRACE)
         r = select_k_smallest(stats, lo, k, ops, comm)
         if ev:
             host_marks.append(time.perf_counter())
         return r
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    _barrier(world)
-    torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -248,6 +253,14 @@ def run_ours(args):
     gc.collect()
     gc.disable()
     with ClockSampler(local) as clk:
+        # warm-up under the same conditions as the timed steps (sampler
+        # running, collector off): the first steps after those start showed
+        # a one-off host stall of 2-100 ms
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        _barrier(world)
+        torch.cuda.synchronize()
         t_start.record(stream)
         marks[0].record(stream)
         for i in range(args.steps):
@@ -261,6 +274,10 @@ def run_ours(args):
               "pass1 ms:", [round(a.elapsed_time(b), 2) for a, b in evs],
               "host select ms:", [round(1e3 * (host_marks[2 * i + 1] - host_marks[2 * i]), 1) for i in range(args.steps)],
               file=sys.stderr)
+        for i, tr in enumerate(step_traces):
+            t0 = host_marks[2 * i]
+            print(f"step {i} select trace (ms after pass-1 launch):",
+                  " ".join(f"{lab}={1e3 * (t - t0):.1f}" for lab, t in tr), file=sys.stderr)
     _barrier(world)
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end) / args.steps

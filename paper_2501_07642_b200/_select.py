@@ -118,6 +118,17 @@ def default_comm():
     return LocalComm()
 
 
+# debug hook (tools / bench FRR_BENCH_DEBUG): (label, perf_counter) marks
+TRACE = None
+
+
+def _mark(label):
+    if TRACE is not None:
+        import time
+
+        TRACE.append((label, time.perf_counter()))
+
+
 SAMPLE = 1 << 20          # statistics sampled to bound the threshold from above
 PREFILTER_MIN = 1 << 22   # global candidate count from which the narrowing pays
 PREFILTER_MAX_Q = 0.05    # acceptance fractions above this select on the full data
@@ -144,7 +155,10 @@ def _upper_bound_bits(stats, k: int, m_total: int, ops, comm):
     st = ops.init(k_s, sample.device)
     for p in range(8):
         ops.pick(ops.hist(sample, st, p), st, p)
-    return int(st[0].item()) & ((1 << 64) - 1), k_s / s
+    _mark("bound launched")
+    h = int(st[0].item()) & ((1 << 64) - 1)
+    _mark("bound read")
+    return h, k_s / s
 
 
 def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool = True):
@@ -172,7 +186,9 @@ def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool
         m = int(stats.shape[0])
         cap = int(qh * m * 1.25) + 4096
         c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, cap)
+        _mark("compact launched")
         n_c = int(c_n.item())
+        _mark("compact read")
         if n_c > c_idx.shape[0]:
             c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, n_c)
         tot = c_n.clone()
@@ -202,7 +218,9 @@ def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
         quota = torch.clamp(ops.k_rem(st) - before, min=0)
         quota = torch.minimum(quota, eq[comm.rank : comm.rank + 1]).contiguous()
     idx, val, n_out = ops.compact(stats, index_base, st, quota, cap=k)
+    _mark("final launched")
     thr = ops.threshold(st)
+    _mark("final read")
     if idx_map is not None:
         idx = idx_map[idx[: int(n_out.item())]]
     if comm.world == 1:
