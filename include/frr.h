@@ -95,6 +95,20 @@ int frr_exact_stats(const frr_balance_t* bal, uint64_t rank_lo, int64_t count, d
  * apply and for regenerated accepted ranks). */
 int frr_exact_stats_ids(const frr_balance_t* bal, const uint64_t* ranks, int64_t m, double* stats,
                         void* stream);
+/* Split enumeration of exact mode (halves of <= 24 units, d <= 16): the host
+ * plan lists the runs of ranks that share their units below na = n/2
+ * (blocks, in rank order: base rank, lower-half mask, offset of the block's
+ * upper-half subsets in lb, the lexicographic s-subset lists grouped by s).
+ * frr_subset_sums builds SA[lower mask] and SB[j] = sum of the rows of the
+ * upper subset lb[j] (rows of `width` = frr_exact_split_width(d) int64);
+ * the S of a rank is SA[lower] + SB[offset + position in the block].  Same
+ * results as frr_exact_stats.  Replaces generation.py:257-272 + 293-296. */
+int frr_exact_split_width(int d);
+int frr_subset_sums(const frr_balance_t* bal, int na, int width, const int32_t* lb, int64_t* sa, int64_t* sb,
+                    void* stream);
+int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
+                          const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base, int64_t nblk,
+                          uint64_t rank_lo, int64_t count, double* stats, void* stream);
 /* Path-forcing variants of frr_mc_stats (frr_mc_stats dispatches): the
  * CUDA-core warp path and the tcgen05 tensor-core path (FRR_E_UNSUPPORTED
  * when the shape or limbs do not fit it). */

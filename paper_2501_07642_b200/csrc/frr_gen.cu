@@ -373,6 +373,90 @@ __global__ void __launch_bounds__(kThreads) k_exact_small(frr_balance_t bal, uin
     }
 }
 
+// ------------------------------------------- exact: split enumeration
+// itertools.combinations order split at na = n/2: a combination is (a, b)
+// with a = its units < na and b = its units >= na, and all combinations
+// sharing a are one contiguous run of ranks in which b runs through the
+// |b|-subsets of the upper units in lexicographic order.  The host plan
+// (generation.py, _split_plan) lists those blocks in rank order (base rank,
+// a, offset of the |b|-subset list), so a rank is (block, offset) and its
+// exact S is SA[a] + SB[b] from two subset-sum tables: two table loads and
+// D integer adds per candidate, no divergent successor walk.
+template <int D>
+__global__ void __launch_bounds__(256) k_subset_sums(const int64_t* __restrict__ zq, int n, int d, int na,
+                                                     const int32_t* __restrict__ lb, int64_t* __restrict__ sa,
+                                                     int64_t* __restrict__ sb) {
+    const int nb = n - na;
+    const int64_t ta = 1ll << na, tot = ta + (1ll << nb);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const bool isa = i < ta;
+        // SA by lower-half mask; SB row j = the upper-half subset lb[j] (the
+        // lexicographic subset lists), so a block's ranks read SB rows in order
+        const int64_t m = isa ? i : (int64_t)lb[i - ta];
+        int64_t* dst = (isa ? sa + i * D : sb + (i - ta) * D);
+        const int off = isa ? 0 : na, nbits = isa ? na : nb;
+        int64_t S[D];
+#pragma unroll
+        for (int u = 0; u < D; u++) S[u] = 0;
+        for (int j = 0; j < nbits; j++)
+            if ((m >> j) & 1) {
+#pragma unroll
+                for (int u = 0; u < D; u++)
+                    if (u < d) S[u] += zq[(size_t)(off + j) * d + u];
+            }
+#pragma unroll
+        for (int u = 0; u < D; u++) dst[u] = S[u];
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const int64_t* __restrict__ sa,
+                                                     const int64_t* __restrict__ sb, const int32_t* __restrict__ blk_a,
+                                                     const int64_t* __restrict__ blk_off,
+                                                     const int64_t* __restrict__ blk_base, int64_t nblk,
+                                                     uint64_t rank_lo, int64_t count, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t chunk = (count + nwarps - 1) / nwarps;
+    chunk = (chunk + 31) & ~(int64_t)31;
+    const int64_t c0 = warp * chunk;
+    if (c0 >= count) return;
+    const int64_t c1 = min(count, c0 + chunk);
+    // block of the warp's first rank (last base <= rank), then per lane
+    int64_t b = 0;
+    if (lane == 0) {
+        const int64_t r = (int64_t)(rank_lo + (uint64_t)c0);
+        int64_t lo = 0, hi = nblk - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (blk_base[mid] <= r) lo = mid;
+            else hi = mid - 1;
+        }
+        b = lo;
+    }
+    b = __shfl_sync(FRR_FULL, b, 0);
+    int64_t base = -1, next = -1, loff = 0;
+    int64_t A[D];
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
+        const int64_t r = (int64_t)(rank_lo + (uint64_t)c);
+        if (r >= next) {
+            while (b + 1 < nblk && blk_base[b + 1] <= r) b++;
+            base = blk_base[b];
+            next = b + 1 < nblk ? blk_base[b + 1] : INT64_MAX;
+            loff = blk_off[b];
+            const int64_t* ar = sa + (int64_t)blk_a[b] * D;
+#pragma unroll
+            for (int u = 0; u < D; u++) A[u] = ar[u];
+        }
+        const int64_t* br = sb + (loff + (r - base)) * D;  // consecutive ranks: consecutive rows
+        int64_t S[D];
+#pragma unroll
+        for (int u = 0; u < D; u++) S[u] = A[u] + br[u];
+        out[c] = small_stat<D>(S, bal.d, bal.g, bal.cc, bal.cst);
+    }
+}
+
 // ------------------------------------------------ randomization-test rows
 // inference.py:82-101 (_dim_rows) for y (a) and for the observed assignment
 // as outcome (b, exact popcounts), plus the pool-membership flag
@@ -706,6 +790,28 @@ int launch_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows, int64_t m
                           ids, rows, m, n, t, y, obs, a, b, match);
 }
 
+int split_width(int d) { return d <= 4 ? 4 : d <= 6 ? 6 : d <= 8 ? 8 : d <= 16 ? 16 : 0; }
+
+template <int D>
+int launch_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, const int32_t* blk_a,
+                 const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
+                 double* out, void* stream) {
+    auto kern = k_exact_split<D>;
+    int rc = frr_prepare_kernel(kern, 0);
+    if (rc) return rc;
+    int grid = frr_persistent_grid(kern, 256, 0, frr_cdiv(count, (int64_t)256 * 32));
+    kern<<<grid, 256, 0, frr_stream(stream)>>>(*bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, out);
+    return frr_check_launch("k_exact_split");
+}
+
+template <int D>
+int launch_subset_sums(const frr_balance_t* bal, int na, const int32_t* lb, int64_t* sa, int64_t* sb, void* stream) {
+    const int64_t tot = (1ll << na) + (1ll << (bal->n - na));
+    k_subset_sums<D><<<(int)std::min<int64_t>(frr_cdiv(tot, 256), 4096), 256, 0, frr_stream(stream)>>>(
+        bal->zq, bal->n, bal->d, na, lb, sa, sb);
+    return frr_check_launch("k_subset_sums");
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -741,6 +847,45 @@ extern "C" int frr_exact_stats_ids(const frr_balance_t* bal, const uint64_t* ran
                                    void* stream) {
     if (!bal) return FRR_E_INVALID_DESIGN;
     return launch_stats<SRC_RANKS>(bal, 0, ranks, nullptr, 0, m, stats, stream);
+}
+
+extern "C" int frr_exact_split_width(int d) { return split_width(d); }
+
+extern "C" int frr_subset_sums(const frr_balance_t* bal, int na, int width, const int32_t* lb, int64_t* sa,
+                               int64_t* sb, void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (width != split_width(bal->d) || na < 1 || na > 24 || bal->n - na < 1 || bal->n - na > 24) {
+        frr_set_error("frr_subset_sums: width %d / halves %d+%d unsupported for d=%d", width, na, bal->n - na, bal->d);
+        return FRR_E_UNSUPPORTED;
+    }
+    switch (width) {
+        case 4: return launch_subset_sums<4>(bal, na, lb, sa, sb, stream);
+        case 6: return launch_subset_sums<6>(bal, na, lb, sa, sb, stream);
+        case 8: return launch_subset_sums<8>(bal, na, lb, sa, sb, stream);
+        default: return launch_subset_sums<16>(bal, na, lb, sa, sb, stream);
+    }
+}
+
+extern "C" int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
+                                     const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base,
+                                     int64_t nblk, uint64_t rank_lo, int64_t count, double* stats, void* stream) {
+    if (!bal) return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (count <= 0) return FRR_OK;
+    if (width != split_width(bal->d) || nblk < 1) {
+        frr_set_error("frr_exact_stats_split: width %d for d=%d, %lld blocks", width, bal->d, (long long)nblk);
+        return FRR_E_UNSUPPORTED;
+    }
+    switch (width) {
+        case 4: return launch_split<4>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
+        case 6: return launch_split<6>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
+        case 8: return launch_split<8>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
+        default:
+            return launch_split<16>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
+    }
 }
 
 extern "C" int frr_rows_stats(const frr_balance_t* bal, const int8_t* rows, int64_t m, double* stats,

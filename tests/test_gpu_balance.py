@@ -103,9 +103,15 @@ def test_mc_stats_vs_oracle(n, d, t, mode, path, monkeypatch):
     assert bits_equal(st, O.c_mc_stats(bal, t, design.root_seed, lo, M))
 
 
-@pytest.mark.parametrize("n,t,d", [(20, 10, 5), (34, 17, 5), (12, 6, 3), (26, 13, 16), (24, 12, 20), (64, 3, 4),
-                                   (80, 2, 5), (18, 9, 1)])
-def test_exact_stats_vs_oracle(n, t, d):
+EXACT_CASES = [(20, 10, 5), (34, 17, 5), (12, 6, 3), (26, 13, 16), (24, 12, 20), (64, 3, 4), (80, 2, 5), (18, 9, 1),
+               # split enumeration corners: t near 0 / n, odd n, widths 4/8/16
+               (25, 1, 4), (25, 24, 7), (31, 5, 8), (36, 30, 12), (35, 18, 6), (24, 23, 16)]
+
+
+@pytest.mark.parametrize("n,t,d", EXACT_CASES)
+@pytest.mark.parametrize("path", ["auto", "successor"])
+def test_exact_stats_vs_oracle(n, t, d, path, monkeypatch):
+    monkeypatch.setenv("FRR_EXACT_PATH", path)
     X = np.random.default_rng(n + d).standard_normal((n, d))
     kern = frr.precompute_precision(X, "ridge")._kernel
     total = math.comb(n, t)
@@ -114,6 +120,10 @@ def test_exact_stats_vs_oracle(n, t, d):
     st = G.exact_stats_device(kern, design, lo, total - lo).cpu().numpy()
     bal = O.Balance(kern._zq, kern._inv_scale_sq)
     assert bits_equal(st, O.c_exact_stats(bal, t, lo, total - lo))
+    if total > 500_000:  # also a window in the middle of the enumeration (block boundaries)
+        mid = total // 2 - 77_777
+        st = G.exact_stats_device(kern, design, mid, 150_001).cpu().numpy()
+        assert bits_equal(st, O.c_exact_stats(bal, t, mid, 150_001))
 
 
 @pytest.mark.parametrize("K,Nn", [(32, 16), (128, 64), (256, 192), (512, 256)])
