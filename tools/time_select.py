@@ -21,3 +21,13 @@ for pf in (True, False):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
     print(f"prefilter={pf}: {dt * 1e3:.2f} ms, k={idx.numel()}")
+import cProfile  # noqa: E402
+import pstats  # noqa: E402
+
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(10):
+    select_k_smallest(st, 0, M // 1000, ops, LocalComm())
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(12)
