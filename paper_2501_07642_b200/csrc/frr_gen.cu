@@ -457,6 +457,47 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
     }
 }
 
+// ------------------------------------------ exact rows, thread per rank
+// n <= 64: each thread unranks its rank into a unit mask (the combinadic
+// walk of k_exact_small), a warp stages its 32 rows in shared memory and
+// writes them as one contiguous, coalesced span.
+constexpr int kRowsThreads = 256;
+__global__ void __launch_bounds__(kRowsThreads) k_exact_rows_small(const uint64_t* __restrict__ ranks, int64_t m,
+                                                                 int n, int t, int8_t* __restrict__ rows) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nb = n + 1;
+    uint64_t* binom = reinterpret_cast<uint64_t*>(smem);                     // [n+1][n+1]
+    unsigned char* stage = reinterpret_cast<unsigned char*>(binom + nb * nb);  // [warps][32 * n]
+    for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) binom[i] = frr_binom(i / nb, i % nb);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* st = stage + (size_t)warp * 32 * n;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; w0 < m; w0 += nwarps * 32) {
+        const int64_t c = w0 + lane;
+        if (c < m) {
+            uint64_t rank = ranks[c], msk = 0;
+            int x = 0;
+            for (int i = 0; i < t; i++) {
+                for (;;) {
+                    const uint64_t cnk = binom[(n - x - 1) * nb + (t - i - 1)];
+                    if (rank < cnk) break;
+                    rank -= cnk;
+                    x++;
+                }
+                msk |= 1ull << x;
+                x++;
+            }
+            for (int e = 0; e < n; e++) st[lane * n + e] = (unsigned char)((msk >> e) & 1);
+        }
+        __syncwarp();
+        const int nrow = m - w0 < 32 ? (int)(m - w0) : 32;
+        int8_t* dst = rows + (size_t)w0 * n;
+        for (int o = lane; o < nrow * n; o += 32) dst[o] = (int8_t)st[o];
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------ randomization-test rows
 // inference.py:82-101 (_dim_rows) for y (a) and for the observed assignment
 // as outcome (b, exact popcounts), plus the pool-membership flag
@@ -907,6 +948,14 @@ extern "C" int frr_regen_mc(uint64_t root_seed, const uint64_t* draws, int64_t m
 
 extern "C" int frr_regen_exact(const uint64_t* ranks, int64_t m, int n, int t, int8_t* rows, uint32_t* bits,
                                void* stream) {
+    if (rows && !bits && n <= 64 && m > 0 && check_nt(n, t) == FRR_OK) {
+        const size_t smem = (size_t)(n + 1) * (n + 1) * sizeof(uint64_t) + (size_t)(kRowsThreads / 32) * 32 * n;
+        int rc = frr_prepare_kernel(k_exact_rows_small, smem);
+        if (rc) return rc;
+        int grid = frr_persistent_grid(k_exact_rows_small, kRowsThreads, smem, frr_cdiv(m, (int64_t)kRowsThreads));
+        k_exact_rows_small<<<grid, kRowsThreads, smem, frr_stream(stream)>>>(ranks, m, n, t, rows);
+        return frr_check_launch("k_exact_rows_small");
+    }
     return launch_regen<SRC_RANKS>(0, ranks, m, n, t, rows, bits, stream);
 }
 

@@ -96,3 +96,21 @@ def test_rejection_keys_golden(golden, case):
     seed, draw = int(g["seeds"][case]), int(g["draw"])
     draws = np.array([draw, draw + 1, 0], dtype=np.uint64)
     assert np.array_equal(frr.batch_assignments(seed, draws, n, t), unpack(g[f"bits_{case}"], n))
+
+
+@pytest.mark.parametrize("n,t", [(2, 1), (20, 10), (34, 17), (33, 1), (40, 39), (64, 32), (64, 3), (66, 33)])
+def test_exact_rows_vs_oracle(n, t):
+    """Accepted-rank regeneration (frr_regen_exact: thread-per-rank rows for
+    n <= 64, the warp path above) against the oracle's combinadic unranking."""
+    import math
+
+    from paper_2501_07642_b200 import generation as G
+
+    total = math.comb(n, t)
+    rng = np.random.default_rng(n * 7 + t)
+    m = min(total, 5001)
+    hi = min(total, 2**62)
+    ranks = np.unique(np.concatenate([np.array([0, hi - 1], dtype=np.uint64),
+                                      rng.integers(0, hi, size=m, dtype=np.uint64)]))
+    got = G.exact_rows_device(ranks, n, t).cpu().numpy()
+    assert np.array_equal(got, O.c_exact_rows(ranks, n, t))
