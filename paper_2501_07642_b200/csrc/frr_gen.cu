@@ -449,10 +449,15 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
 #pragma unroll
             for (int u = 0; u < D; u++) A[u] = ar[u];
         }
-        const int64_t* br = sb + (loff + (r - base)) * D;  // consecutive ranks: consecutive rows
+        // consecutive ranks: consecutive rows (D * 8 bytes, a multiple of 16)
+        const longlong2* br = reinterpret_cast<const longlong2*>(sb + (loff + (r - base)) * D);
         int64_t S[D];
 #pragma unroll
-        for (int u = 0; u < D; u++) S[u] = A[u] + br[u];
+        for (int u = 0; u < D / 2; u++) {
+            const longlong2 v = __ldg(br + u);
+            S[2 * u] = A[2 * u] + v.x;
+            S[2 * u + 1] = A[2 * u + 1] + v.y;
+        }
         out[c] = small_stat<D>(S, bal.d, bal.g, bal.cc, bal.cst);
     }
 }
