@@ -130,35 +130,63 @@ __global__ void __launch_bounds__(kCThreads) k_tile_counts(const uint64_t* __res
 }
 
 // exclusive scan of the tile counts (single CTA), total accepted count
+// Exclusive scan of the per-tile (below, tie) counts, one CTA: 4096 tiles
+// per round, 4 per thread, warp-shuffle scans, one shared-memory step for the
+// warp totals (2 barriers per round instead of 20).
+__device__ __forceinline__ void warp_incl_scan2(int64_t& a, int64_t& b, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t va = __shfl_up_sync(0xffffffffu, a, o), vb = __shfl_up_sync(0xffffffffu, b, o);
+        if (lane >= o) {
+            a += va;
+            b += vb;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_tile_scan(int64_t* ws, int64_t ntiles, const int64_t* tie_quota,
                                                     int64_t* n_out) {
-    __shared__ int64_t s_a[1024], s_b[1024];
-    __shared__ int64_t carry_a, carry_b;
-    if (threadIdx.x == 0) carry_a = carry_b = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < ntiles; base += 1024) {
-        int64_t i = base + threadIdx.x;
-        int64_t a = i < ntiles ? ws[2 * i] : 0, b = i < ntiles ? ws[2 * i + 1] : 0;
-        s_a[threadIdx.x] = a;
-        s_b[threadIdx.x] = b;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            int64_t va = threadIdx.x >= o ? s_a[threadIdx.x - o] : 0;
-            int64_t vb = threadIdx.x >= o ? s_b[threadIdx.x - o] : 0;
-            __syncthreads();
-            s_a[threadIdx.x] += va;
-            s_b[threadIdx.x] += vb;
-            __syncthreads();
+    __shared__ int64_t s_wa[32], s_wb[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t carry_a = 0, carry_b = 0;  // identical in every thread
+    for (int64_t base = 0; base < ntiles; base += 4096) {
+        const int64_t i0 = base + 4 * (int64_t)threadIdx.x;
+        int64_t a[4], b[4], ta = 0, tb = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const bool ok = i0 + u < ntiles;
+            a[u] = ok ? ws[2 * (i0 + u)] : 0;
+            b[u] = ok ? ws[2 * (i0 + u) + 1] : 0;
+            ta += a[u];
+            tb += b[u];
         }
-        if (i < ntiles) {
-            ws[2 * i] = carry_a + s_a[threadIdx.x] - a;
-            ws[2 * i + 1] = carry_b + s_b[threadIdx.x] - b;
+        int64_t ia = ta, ib = tb;
+        warp_incl_scan2(ia, ib, lane);
+        if (lane == 31) {
+            s_wa[warp] = ia;
+            s_wb[warp] = ib;
         }
         __syncthreads();
-        if (threadIdx.x == 1023) {
-            carry_a += s_a[1023];
-            carry_b += s_b[1023];
+        if (warp == 0) {
+            int64_t wa = s_wa[lane], wb = s_wb[lane];
+            warp_incl_scan2(wa, wb, lane);
+            s_wa[lane] = wa;
+            s_wb[lane] = wb;
         }
+        __syncthreads();
+        int64_t ea = carry_a + (warp ? s_wa[warp - 1] : 0) + ia - ta;
+        int64_t eb = carry_b + (warp ? s_wb[warp - 1] : 0) + ib - tb;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (i0 + u < ntiles) {
+                ws[2 * (i0 + u)] = ea;
+                ws[2 * (i0 + u) + 1] = eb;
+            }
+            ea += a[u];
+            eb += b[u];
+        }
+        carry_a += s_wa[31];
+        carry_b += s_wb[31];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
