@@ -66,7 +66,7 @@ for f in handles:
 # box are erratic (power ramp); launch the first build until AB_WARM seconds pass
 import time  # noqa: E402
 
-t_warm = time.time() + float(os.environ.get("AB_WARM", "2"))
+t_warm = time.time() + float(os.environ.get("AB_WARM", "5"))
 while time.time() < t_warm:
     launch(handles[0])
     torch.cuda.synchronize()
