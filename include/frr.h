@@ -109,6 +109,17 @@ int frr_subset_sums(const frr_balance_t* bal, int na, int width, const int32_t* 
 int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
                           const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base, int64_t nblk,
                           uint64_t rank_lo, int64_t count, double* stats, void* stream);
+/* frr_exact_stats_split fused with the select's narrowing step: no
+ * statistics array; the (rank, statistic) pairs whose statistic's IEEE bits
+ * are <= h_bits are appended, in no particular order, to idx/vals (at most
+ * cap written) and *n_kept (caller-zeroed, accumulates over launches) counts
+ * them all.  The caller sorts by rank and runs the radix select on them
+ * (same accepted set as generation.py:159-169 whenever >= k statistics are
+ * kept and *n_kept <= cap; otherwise it falls back to the full array). */
+int frr_exact_stats_split_filtered(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
+                                   const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base,
+                                   int64_t nblk, uint64_t rank_lo, int64_t count, uint64_t h_bits, int64_t cap,
+                                   int64_t* idx, double* vals, uint64_t* n_kept, void* stream);
 /* Path-forcing variants of frr_mc_stats (frr_mc_stats dispatches): the
  * CUDA-core warp path and the tcgen05 tensor-core path (FRR_E_UNSUPPORTED
  * when the shape or limbs do not fit it). */

@@ -58,6 +58,8 @@ SIGNATURES = {
     "frr_exact_split_width": (i32, [i32]),
     "frr_subset_sums": (i32, [ctypes.POINTER(Balance), i32, i32, vp, vp, vp, vp]),
     "frr_exact_stats_split": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, vp, vp, i64, u64, i64, vp, vp]),
+    "frr_exact_stats_split_filtered": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, vp, vp, i64, u64, i64, u64,
+                                             i64, vp, vp, vp, vp]),
     "frr_rows_stats": (i32, [ctypes.POINTER(Balance), vp, i64, vp, vp]),
     "frr_regen_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp]),
     "frr_regen_exact": (i32, [vp, i64, i32, i32, vp, vp, vp]),

@@ -140,12 +140,24 @@ def _upper_bound_bits(stats, k: int, m_total: int, ops, comm):
     (same on every rank), k_s = q s + 8 sqrt(q s) + 16 for q = k / M.  A bad
     bound is detected by the caller (fewer than k statistics <= h) and only
     costs a fall back to the full select."""
-    torch = N.torch_mod()
     m = int(stats.shape[0])
-    s_r = max(1, min(m, SAMPLE // comm.world))
+    s_r = sample_size(m, comm)
     stride = max(1, m // s_r)
-    sample = stats[::stride][:s_r].contiguous()
-    if sample.shape[0] < s_r:  # m < s_r * stride cannot happen; keep shapes equal across ranks
+    return bound_from_sample(stats[::stride][:s_r].contiguous(), k, m_total, ops, comm)
+
+
+def sample_size(m: int, comm) -> int:
+    """Per-rank sample length (equal on every rank for shards >= SAMPLE)."""
+    return max(1, min(m, SAMPLE // comm.world))
+
+
+def bound_from_sample(sample, k: int, m_total: int, ops, comm):
+    """(h, fraction) of _upper_bound_bits from this rank's sample of
+    sample_size(m) statistics; the samples of all ranks are gathered so that
+    every rank gets the same h."""
+    torch = N.torch_mod()
+    s_r = sample_size(int(sample.shape[0]), comm) if comm.world == 1 else SAMPLE // comm.world
+    if sample.shape[0] < s_r:  # keep shapes equal across ranks
         sample = torch.cat([sample, sample.new_full((s_r - sample.shape[0],), float("inf"))])
     if comm.world > 1:
         sample = torch.cat(comm.all_gather(sample))

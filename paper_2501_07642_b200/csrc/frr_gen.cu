@@ -409,12 +409,19 @@ __global__ void __launch_bounds__(256) k_subset_sums(const int64_t* __restrict__
     }
 }
 
-template <int D>
+// FILT: instead of writing every statistic, append (rank, stat) of the
+// statistics whose bits are <= hbits (statistics are >= +0, so bit order is
+// value order) to fidx/fval (unordered; warp-aggregated atomic on fcount,
+// entries past cap counted but not written).  The caller sorts by rank.
+template <int D, bool FILT>
 __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const int64_t* __restrict__ sa,
                                                      const int64_t* __restrict__ sb, const int32_t* __restrict__ blk_a,
                                                      const int64_t* __restrict__ blk_off,
                                                      const int64_t* __restrict__ blk_base, int64_t nblk,
-                                                     uint64_t rank_lo, int64_t count, double* __restrict__ out) {
+                                                     uint64_t rank_lo, int64_t count, double* __restrict__ out,
+                                                     uint64_t hbits, int64_t cap, int64_t* __restrict__ fidx,
+                                                     double* __restrict__ fval,
+                                                     unsigned long long* __restrict__ fcount) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -438,27 +445,47 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
     b = __shfl_sync(FRR_FULL, b, 0);
     int64_t base = -1, next = -1, loff = 0;
     int64_t A[D];
-    for (int64_t c = c0 + lane; c < c1; c += 32) {
+    // uniform trip count over the warp (ballot in the filtered variant)
+    for (int64_t cb = c0; cb < c1; cb += 32) {
+        const int64_t c = cb + lane;
+        const bool valid = c < c1;
         const int64_t r = (int64_t)(rank_lo + (uint64_t)c);
-        if (r >= next) {
-            while (b + 1 < nblk && blk_base[b + 1] <= r) b++;
-            base = blk_base[b];
-            next = b + 1 < nblk ? blk_base[b + 1] : INT64_MAX;
-            loff = blk_off[b];
-            const int64_t* ar = sa + (int64_t)blk_a[b] * D;
+        double st = 0.0;
+        if (valid) {
+            if (r >= next) {
+                while (b + 1 < nblk && blk_base[b + 1] <= r) b++;
+                base = blk_base[b];
+                next = b + 1 < nblk ? blk_base[b + 1] : INT64_MAX;
+                loff = blk_off[b];
+                const int64_t* ar = sa + (int64_t)blk_a[b] * D;
 #pragma unroll
-            for (int u = 0; u < D; u++) A[u] = ar[u];
-        }
-        // consecutive ranks: consecutive rows (D * 8 bytes, a multiple of 16)
-        const longlong2* br = reinterpret_cast<const longlong2*>(sb + (loff + (r - base)) * D);
-        int64_t S[D];
+                for (int u = 0; u < D; u++) A[u] = ar[u];
+            }
+            // consecutive ranks: consecutive rows (D * 8 bytes, a multiple of 16)
+            const longlong2* br = reinterpret_cast<const longlong2*>(sb + (loff + (r - base)) * D);
+            int64_t S[D];
 #pragma unroll
-        for (int u = 0; u < D / 2; u++) {
-            const longlong2 v = __ldg(br + u);
-            S[2 * u] = A[2 * u] + v.x;
-            S[2 * u + 1] = A[2 * u + 1] + v.y;
+            for (int u = 0; u < D / 2; u++) {
+                const longlong2 v = __ldg(br + u);
+                S[2 * u] = A[2 * u] + v.x;
+                S[2 * u + 1] = A[2 * u + 1] + v.y;
+            }
+            st = small_stat<D>(S, bal.d, bal.g, bal.cc, bal.cst);
+            if (!FILT) out[c] = st;
         }
-        out[c] = small_stat<D>(S, bal.d, bal.g, bal.cc, bal.cst);
+        if (FILT) {
+            const bool keep = valid && (uint64_t)__double_as_longlong(st) <= hbits;
+            const unsigned m = __ballot_sync(FRR_FULL, keep);
+            if (m) {
+                unsigned long long at = 0;
+                if (lane == 0) at = atomicAdd(fcount, (unsigned long long)__popc(m));
+                at = __shfl_sync(FRR_FULL, at, 0) + __popc(m & ((1u << lane) - 1u));
+                if (keep && at < (unsigned long long)cap) {
+                    fidx[at] = r;
+                    fval[at] = st;
+                }
+            }
+        }
     }
 }
 
@@ -838,16 +865,27 @@ int launch_dim(uint64_t seed, const uint64_t* ids, const int8_t* rows, int64_t m
 
 int split_width(int d) { return d <= 4 ? 4 : d <= 6 ? 6 : d <= 8 ? 8 : d <= 16 ? 16 : 0; }
 
+struct SplitFilter {
+    uint64_t hbits;
+    int64_t cap;
+    int64_t* idx;
+    double* val;
+    unsigned long long* count;
+};
+
 template <int D>
 int launch_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, const int32_t* blk_a,
                  const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
-                 double* out, void* stream) {
-    auto kern = k_exact_split<D>;
+                 double* out, const SplitFilter* f, void* stream) {
+    auto kern = f ? k_exact_split<D, true> : k_exact_split<D, false>;
     int rc = frr_prepare_kernel(kern, 0);
     if (rc) return rc;
     int grid = frr_persistent_grid(kern, 256, 0, frr_cdiv(count, (int64_t)256 * 32));
-    kern<<<grid, 256, 0, frr_stream(stream)>>>(*bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, out);
-    return frr_check_launch("k_exact_split");
+    const SplitFilter z{0, 0, nullptr, nullptr, nullptr};
+    const SplitFilter& F = f ? *f : z;
+    kern<<<grid, 256, 0, frr_stream(stream)>>>(*bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, out,
+                                               F.hbits, F.cap, F.idx, F.val, F.count);
+    return frr_check_launch(f ? "k_exact_split<filtered>" : "k_exact_split");
 }
 
 template <int D>
@@ -856,6 +894,18 @@ int launch_subset_sums(const frr_balance_t* bal, int na, const int32_t* lb, int6
     k_subset_sums<D><<<(int)std::min<int64_t>(frr_cdiv(tot, 256), 4096), 256, 0, frr_stream(stream)>>>(
         bal->zq, bal->n, bal->d, na, lb, sa, sb);
     return frr_check_launch("k_subset_sums");
+}
+
+int split_dispatch(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width, const int32_t* blk_a,
+                   const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
+                   double* stats, const SplitFilter* f, void* stream) {
+    switch (width) {
+        case 4: return launch_split<4>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+        case 6: return launch_split<6>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+        case 8: return launch_split<8>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+        default:
+            return launch_split<16>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+    }
 }
 
 }  // namespace
@@ -925,13 +975,27 @@ extern "C" int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa
         frr_set_error("frr_exact_stats_split: width %d for d=%d, %lld blocks", width, bal->d, (long long)nblk);
         return FRR_E_UNSUPPORTED;
     }
-    switch (width) {
-        case 4: return launch_split<4>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
-        case 6: return launch_split<6>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
-        case 8: return launch_split<8>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
-        default:
-            return launch_split<16>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, stream);
+    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, nullptr,
+                          stream);
+}
+
+extern "C" int frr_exact_stats_split_filtered(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb,
+                                              int width, const int32_t* blk_a, const int64_t* blk_off,
+                                              const int64_t* blk_base, int64_t nblk, uint64_t rank_lo,
+                                              int64_t count, uint64_t h_bits, int64_t cap, int64_t* idx,
+                                              double* vals, uint64_t* n_kept, void* stream) {
+    if (!bal || !n_kept || cap < 0 || (cap > 0 && (!idx || !vals))) return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (count <= 0) return FRR_OK;
+    if (width != split_width(bal->d) || nblk < 1) {
+        frr_set_error("frr_exact_stats_split_filtered: width %d for d=%d, %lld blocks", width, bal->d,
+                      (long long)nblk);
+        return FRR_E_UNSUPPORTED;
     }
+    const SplitFilter f{h_bits, cap, idx, vals, reinterpret_cast<unsigned long long*>(n_kept)};
+    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, nullptr, &f,
+                          stream);
 }
 
 extern "C" int frr_rows_stats(const frr_balance_t* bal, const int8_t* rows, int64_t m, double* stats,

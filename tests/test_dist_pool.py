@@ -55,8 +55,39 @@ CASES = {
 }
 
 
+def _patch_fused(setattr_, variant):
+    """Exact pass 1 fused with the narrowing (generation.exact_narrowed_device)
+    on every shard, whatever its size: the sample and filter kernels replaced
+    by the oracle, the filter's output shuffled (the kernel appends in no
+    particular order).  variant "low": a bound below the threshold, so every
+    rank must agree to fall back to the full statistics."""
+    from paper_2501_07642_b200 import _select as S
+
+    def shard_stats(kernel, design, lo, count):
+        bal = O.Balance(kernel._zq, kernel._inv_scale_sq)
+        return O.c_exact_stats(bal, design.n_treated, lo, count, threads=1)
+
+    def sample(kernel, design, lo, stride, s_r):
+        return torch.from_numpy(shard_stats(kernel, design, lo, stride * s_r)[::stride].copy())
+
+    def filt(kernel, design, lo, count, h, cap):
+        st = shard_stats(kernel, design, lo, count)
+        keep = np.flatnonzero(st.view(np.uint64) <= np.uint64(h))
+        keep = np.random.default_rng(lo).permutation(keep)
+        idx, val = lo + keep[:cap], st[keep[:cap]]
+        return torch.from_numpy(idx.astype(np.int64)), torch.from_numpy(val.copy()), int(keep.size)
+
+    setattr_(G, "_use_fused_select", lambda design, d, m, k: design.mode == "exact")
+    setattr_(G, "_narrow_sample", sample)
+    setattr_(G, "_narrow_filter", filt)
+    setattr_(G, "_select_ops", NumpySelectOps)
+    setattr_(S, "SAMPLE", 600)
+    if variant == "low":
+        setattr_(S, "bound_from_sample", lambda *a: (0, 0.0))
+
+
 def _build(name):
-    X, kw = CASES[name]
+    X, kw = CASES[name.split(":")[0]]
     design = frr.DesignSpec(**kw)
     pool = frr.generate_pool(X, design)
     return (pool.accepted_indices, pool.stats, pool.threshold_value,
@@ -68,6 +99,8 @@ def _worker(rank, world, port, name, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         _patch_compute()
+        if ":" in name:
+            _patch_fused(setattr, name.split(":")[1])
         out[rank] = _build(name)
     finally:
         dist.destroy_process_group()
@@ -97,10 +130,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name,world", [("mc", 2), ("mc_ties", 3), ("exact", 2)])
+@pytest.mark.parametrize("name,world", [("mc", 2), ("mc_ties", 3), ("exact", 2), ("exact:fused", 2),
+                                        ("exact:fused", 3), ("exact:low", 2)])
 def test_sharded_pool_equals_single_rank(name, world, monkeypatch):
     _patch_compute(monkeypatch.setattr)  # restored after the test
-    want = _build(name)  # world size 1 (no process group in this process)
+    want = _build(name.split(":")[0])  # world size 1, unfused (no process group in this process)
     with mp.Manager() as man:
         out = man.dict()
         mp.spawn(_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
@@ -121,3 +155,13 @@ def test_pool_stats_gather_rank_order():
     for r in range(world):
         a, b, match = results[r]
         assert np.array_equal(a, np.arange(1001) * 0.5) and np.array_equal(b, -np.arange(1001.0)) and match == 1
+
+
+def test_fused_exact_single_rank_equals_unfused(monkeypatch):
+    _patch_compute(monkeypatch.setattr)
+    want = _build("exact")
+    _patch_fused(monkeypatch.setattr, "fused")
+    monkeypatch.setattr(G, "exact_stats_device", None)  # the fused path must not need the full array
+    got = _build("exact:fused")
+    assert all(np.array_equal(g, w) for g, w in zip(got[:2], want[:2])) and got[2] == want[2]
+    assert np.array_equal(got[3], want[3])

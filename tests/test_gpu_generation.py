@@ -293,3 +293,61 @@ def test_c3_sampled_parity_around_threshold():
     rows = O.c_batch_assign(43, idx.astype(np.uint64), 2000, 1000)
     want = O.c_stats_rows(bal, rows, 1000)
     assert np.array_equal(st[idx].view(np.uint64), want.view(np.uint64))
+
+
+def _exact_pool_both(X, design, monkeypatch):
+    fused = frr.enumerate_exact(X, design)
+    monkeypatch.setenv("FRR_EXACT_FUSED_SELECT", "0")
+    plain = frr.enumerate_exact(X, design)
+    monkeypatch.delenv("FRR_EXACT_FUSED_SELECT")
+    return fused, plain
+
+
+@pytest.mark.parametrize("integer_x", [False, True])
+def test_fused_exact_select_vs_oracle(monkeypatch, integer_x):
+    """Exact pass 1 fused with the narrowing (frr_exact_stats_split_filtered)
+    against the oracle's full statistics + stable-argsort select, n=24
+    (2,704,156 ranks); integer X makes many statistics tie at the threshold."""
+    from paper_2501_07642_b200 import _select as S
+    monkeypatch.setattr(S, "PREFILTER_MIN", 1 << 20)
+    rng = np.random.default_rng(24)
+    X = rng.integers(-2, 3, size=(24, 5)).astype(np.float64) if integer_x else rng.standard_normal((24, 5))
+    design = frr.DesignSpec(24, 12, accept_prob=2e-3, mode="exact")
+    fused, plain = _exact_pool_both(X, design, monkeypatch)
+    assert G.pools_equal(fused, plain) and np.array_equal(fused.assignments, plain.assignments)
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    st = O.c_exact_stats(bal, 12, 0, math.comb(24, 12))
+    want, wthr = O.c_select(st, 2e-3)
+    assert np.array_equal(fused.accepted_indices, want) and fused.threshold_value == wthr
+    assert np.array_equal(fused.stats, st[want])
+
+
+@pytest.mark.parametrize("bound", ["low", "overflow"])
+def test_fused_exact_select_fallbacks(monkeypatch, bound):
+    """A bound below the threshold (fewer than k kept) or one that keeps
+    more than the buffer holds falls back to the full statistics array."""
+    from paper_2501_07642_b200 import _select as S
+    monkeypatch.setattr(S, "PREFILTER_MIN", 1 << 20)
+    h = 0 if bound == "low" else 0x7FF0000000000000  # +0.0 / +inf
+    monkeypatch.setattr(S, "bound_from_sample", lambda *a: (h, 0.0))
+    calls = []
+    real = G.exact_stats_device
+    monkeypatch.setattr(G, "exact_stats_device", lambda *a, **kw: calls.append(1) or real(*a, **kw))
+    X = np.random.default_rng(3).standard_normal((26, 5))
+    design = frr.DesignSpec(26, 13, accept_prob=1e-3, mode="exact")
+    fused = frr.enumerate_exact(X, design)
+    assert calls == [1]  # the fallback ran pass 1 unfused
+    monkeypatch.undo()
+    monkeypatch.setenv("FRR_EXACT_FUSED_SELECT", "0")
+    plain = frr.enumerate_exact(X, design)
+    assert G.pools_equal(fused, plain)
+
+
+def test_fused_exact_select_n26_matches_unfused(monkeypatch):
+    """n=26, t=13 (10,400,600 ranks): above PREFILTER_MIN with the default
+    constants, so enumerate_exact takes the fused path as C4 does."""
+    X = np.random.default_rng(26).standard_normal((26, 5))
+    design = frr.DesignSpec(26, 13, accept_prob=1e-3, mode="exact")
+    fused, plain = _exact_pool_both(X, design, monkeypatch)
+    assert fused.n_accepted == math.floor(1e-3 * math.comb(26, 13))
+    assert G.pools_equal(fused, plain) and np.array_equal(fused.assignments, plain.assignments)
