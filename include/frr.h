@@ -109,6 +109,12 @@ int frr_subset_sums(const frr_balance_t* bal, int na, int width, const int32_t* 
 int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
                           const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base, int64_t nblk,
                           uint64_t rank_lo, int64_t count, double* stats, void* stream);
+/* frr_exact_stats_split on the sampled ranks rank_lo + j * stride, j < count
+ * (stats[j]); the select's upper bound for the fused path comes from it. */
+int frr_exact_stats_split_strided(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
+                                  const int32_t* blk_a, const int64_t* blk_off, const int64_t* blk_base,
+                                  int64_t nblk, uint64_t rank_lo, int64_t stride, int64_t count, double* stats,
+                                  void* stream);
 /* frr_exact_stats_split fused with the select's narrowing step: no
  * statistics array; the (rank, statistic) pairs whose statistic's IEEE bits
  * are <= h_bits are appended, in no particular order, to idx/vals (at most

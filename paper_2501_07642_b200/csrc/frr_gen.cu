@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
                                                      uint64_t rank_lo, int64_t count, double* __restrict__ out,
                                                      uint64_t hbits, int64_t cap, int64_t* __restrict__ fidx,
                                                      double* __restrict__ fval,
-                                                     unsigned long long* __restrict__ fcount) {
+                                                     unsigned long long* __restrict__ fcount, int64_t stride) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
     // block of the warp's first rank (last base <= rank), then per lane
     int64_t b = 0;
     if (lane == 0) {
-        const int64_t r = (int64_t)(rank_lo + (uint64_t)c0);
+        const int64_t r = (int64_t)(rank_lo + (uint64_t)c0 * (uint64_t)stride);
         int64_t lo = 0, hi = nblk - 1;
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
@@ -449,10 +449,19 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
     for (int64_t cb = c0; cb < c1; cb += 32) {
         const int64_t c = cb + lane;
         const bool valid = c < c1;
-        const int64_t r = (int64_t)(rank_lo + (uint64_t)c);
+        const int64_t r = (int64_t)(rank_lo + (uint64_t)c * (uint64_t)stride);
         double st = 0.0;
         if (valid) {
             if (r >= next) {
+                if (stride > 1) {  // sampled ranks: each one may be many blocks further
+                    int64_t lo = b, hi = nblk - 1;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi + 1) >> 1;
+                        if (blk_base[mid] <= r) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    b = lo;
+                }
                 while (b + 1 < nblk && blk_base[b + 1] <= r) b++;
                 base = blk_base[b];
                 next = b + 1 < nblk ? blk_base[b + 1] : INT64_MAX;
@@ -876,7 +885,7 @@ struct SplitFilter {
 template <int D>
 int launch_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, const int32_t* blk_a,
                  const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
-                 double* out, const SplitFilter* f, void* stream) {
+                 double* out, const SplitFilter* f, int64_t stride, void* stream) {
     auto kern = f ? k_exact_split<D, true> : k_exact_split<D, false>;
     int rc = frr_prepare_kernel(kern, 0);
     if (rc) return rc;
@@ -884,7 +893,7 @@ int launch_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb,
     const SplitFilter z{0, 0, nullptr, nullptr, nullptr};
     const SplitFilter& F = f ? *f : z;
     kern<<<grid, 256, 0, frr_stream(stream)>>>(*bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, out,
-                                               F.hbits, F.cap, F.idx, F.val, F.count);
+                                               F.hbits, F.cap, F.idx, F.val, F.count, stride);
     return frr_check_launch(f ? "k_exact_split<filtered>" : "k_exact_split");
 }
 
@@ -898,13 +907,13 @@ int launch_subset_sums(const frr_balance_t* bal, int na, const int32_t* lb, int6
 
 int split_dispatch(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width, const int32_t* blk_a,
                    const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
-                   double* stats, const SplitFilter* f, void* stream) {
+                   double* stats, const SplitFilter* f, int64_t stride, void* stream) {
     switch (width) {
-        case 4: return launch_split<4>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
-        case 6: return launch_split<6>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
-        case 8: return launch_split<8>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+        case 4: return launch_split<4>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stride, stream);
+        case 6: return launch_split<6>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stride, stream);
+        case 8: return launch_split<8>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stride, stream);
         default:
-            return launch_split<16>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stream);
+            return launch_split<16>(bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, f, stride, stream);
     }
 }
 
@@ -975,7 +984,24 @@ extern "C" int frr_exact_stats_split(const frr_balance_t* bal, const int64_t* sa
         frr_set_error("frr_exact_stats_split: width %d for d=%d, %lld blocks", width, bal->d, (long long)nblk);
         return FRR_E_UNSUPPORTED;
     }
-    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, nullptr,
+    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, nullptr, 1,
+                          stream);
+}
+
+extern "C" int frr_exact_stats_split_strided(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb,
+                                             int width, const int32_t* blk_a, const int64_t* blk_off,
+                                             const int64_t* blk_base, int64_t nblk, uint64_t rank_lo,
+                                             int64_t stride, int64_t count, double* stats, void* stream) {
+    if (!bal || stride < 1) return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (count <= 0) return FRR_OK;
+    if (width != split_width(bal->d) || nblk < 1) {
+        frr_set_error("frr_exact_stats_split_strided: width %d for d=%d, %lld blocks", width, bal->d,
+                      (long long)nblk);
+        return FRR_E_UNSUPPORTED;
+    }
+    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, stats, nullptr, stride,
                           stream);
 }
 
@@ -994,7 +1020,7 @@ extern "C" int frr_exact_stats_split_filtered(const frr_balance_t* bal, const in
         return FRR_E_UNSUPPORTED;
     }
     const SplitFilter f{h_bits, cap, idx, vals, reinterpret_cast<unsigned long long*>(n_kept)};
-    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, nullptr, &f,
+    return split_dispatch(bal, sa, sb, width, blk_a, blk_off, blk_base, nblk, rank_lo, count, nullptr, &f, 1,
                           stream);
 }
 

@@ -351,3 +351,36 @@ def test_fused_exact_select_n26_matches_unfused(monkeypatch):
     fused, plain = _exact_pool_both(X, design, monkeypatch)
     assert fused.n_accepted == math.floor(1e-3 * math.comb(26, 13))
     assert G.pools_equal(fused, plain) and np.array_equal(fused.assignments, plain.assignments)
+
+
+@pytest.mark.parametrize("n,t,lo,stride", [(34, 17, 0, 2225), (34, 17, 123_456_789, 999_983), (26, 13, 5, 1),
+                                           (27, 9, 17, 4099)])
+def test_split_strided_sample_vs_oracle(n, t, lo, stride):
+    """The fused path's sample kernel: statistics of ranks lo + j * stride."""
+    import paper_2501_07642_b200._native as NAT
+    X = np.random.default_rng(n + t).standard_normal((n, 5))
+    design = frr.DesignSpec(n, t, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    kern = frr.precompute_precision(X, "exact")._kernel
+    m = min(4096, (math.comb(n, t) - lo + stride - 1) // stride)
+    got = G._narrow_sample(kern, design, lo, stride, m).cpu().numpy()
+    bal = O.balance_setup(X, O.precision(X, "exact"))
+    ranks = lo + stride * np.arange(m, dtype=np.uint64)
+    rows = O.c_exact_rows(ranks.astype(np.uint64), n, t)
+    assert np.array_equal(got, O.c_stats_rows(bal, rows, t))
+    assert NAT.lib().frr_exact_stats_split_strided  # exported
+
+
+@pytest.mark.parametrize("shape,dtype", [((2333606, 34), "int8"), ((2333606,), "int64"), (((1 << 18) + 3,), "float64"),
+                                         ((77, 3), "int8"), ((40_000_001,), "float64")])
+def test_staged_to_host_pipelined(shape, dtype):
+    """_native.to_host (chunked DMA through the page-locked stage, host copies
+    overlapped) returns exactly the tensor's contents."""
+    import torch
+    import paper_2501_07642_b200._native as NAT
+    g = torch.Generator(device="cuda").manual_seed(7)
+    t = torch.randint(-100, 100, shape, dtype=getattr(torch, dtype), device="cuda", generator=g)
+    if dtype == "float64":
+        t = t * 0.37
+    for _ in range(2):
+        got = NAT.to_host(t)
+        assert got.dtype == t.cpu().numpy().dtype and np.array_equal(got, t.cpu().numpy())
