@@ -60,6 +60,8 @@ SIGNATURES = {
     "frr_exact_stats_split": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, vp, vp, i64, u64, i64, vp, vp]),
     "frr_exact_stats_split_strided": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, vp, vp, i64, u64, i64, i64,
                                             vp, vp]),
+    "frr_exact_tiled_filtered": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, i64, vp, vp, u64, u64, u64, i64,
+                                       vp, vp, vp, vp]),
     "frr_exact_stats_split_filtered": (i32, [ctypes.POINTER(Balance), vp, vp, i32, vp, vp, vp, i64, u64, i64, u64,
                                              i64, vp, vp, vp, vp]),
     "frr_rows_stats": (i32, [ctypes.POINTER(Balance), vp, i64, vp, vp]),

@@ -498,6 +498,78 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
     }
 }
 
+// ------------------------------------ split enumeration, tiled (filtered)
+// The same (lower, upper) decomposition as k_exact_split, reordered for
+// reuse: a tile pairs up to kTileRows consecutive upper-half subsets of one
+// size s (SB rows j0 .. j0+nrows, held in registers, one per thread) with
+// up to kTileBlocks blocks of that s (their SA rows staged in shared memory
+// and read as warp broadcasts).  Candidate (block g, row j) has rank
+// base_g + j.  Every SB row is loaded once per tile instead of once per
+// candidate, so the kernel is bound by the fp64 epilogue, not by L2.  Only
+// the filtered output exists (ranks come out in tile order; the caller
+// sorts).  tiles[i] = {sb_row0, j0 << 32 | nrows, g0, ng}.
+constexpr int kTileRows = 256, kTileBlocks = 256;
+
+template <int D, int DD>  // DD = d, a compile-time constant: no per-column predicates in the epilogue
+__global__ void __launch_bounds__(kTileRows) k_exact_tiled(frr_balance_t bal, const int64_t* __restrict__ sa,
+                                                           const int64_t* __restrict__ sb,
+                                                           const int64_t* __restrict__ tiles, int64_t ntiles,
+                                                           const int32_t* __restrict__ g_a,
+                                                           const int64_t* __restrict__ g_base, int64_t rank_lo,
+                                                           int64_t rank_hi, uint64_t hbits, int64_t cap,
+                                                           int64_t* __restrict__ fidx, double* __restrict__ fval,
+                                                           unsigned long long* __restrict__ fcount) {
+    __shared__ __align__(16) int64_t sA[kTileBlocks * D];
+    __shared__ int64_t sBase[kTileBlocks];
+    const int lane = threadIdx.x & 31;
+    double ccr[D];
+#pragma unroll
+    for (int u = 0; u < D; u++) ccr[u] = u < DD ? bal.cc[u] : 0.0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t sb_row0 = tiles[4 * tile], jn = tiles[4 * tile + 1], g0 = tiles[4 * tile + 2];
+        const int ng = (int)tiles[4 * tile + 3];
+        const int nrows = (int)(jn & 0xFFFFFFFF);
+        const int64_t j = (jn >> 32) + threadIdx.x;
+        __syncthreads();  // previous tile's readers are done with sA
+        for (int i = threadIdx.x; i < ng * D; i += blockDim.x) sA[i] = sa[(int64_t)g_a[g0 + i / D] * D + i % D];
+        for (int i = threadIdx.x; i < ng; i += blockDim.x) sBase[i] = g_base[g0 + i];
+        const bool row_ok = threadIdx.x < nrows;
+        int64_t B[D];
+        const longlong2* br = reinterpret_cast<const longlong2*>(sb + (sb_row0 + (row_ok ? threadIdx.x : 0)) * D);
+#pragma unroll
+        for (int u = 0; u < D / 2; u++) {
+            const longlong2 v = __ldg(br + u);
+            B[2 * u] = v.x;
+            B[2 * u + 1] = v.y;
+        }
+        __syncthreads();
+        for (int g = 0; g < ng; g++) {
+            const int64_t r = sBase[g] + j;
+            const bool valid = row_ok && r >= rank_lo && r < rank_hi;
+            const longlong2* ar = reinterpret_cast<const longlong2*>(sA + g * D);
+            int64_t S[D];
+#pragma unroll
+            for (int u = 0; u < D / 2; u++) {
+                const longlong2 a = ar[u];
+                S[2 * u] = a.x + B[2 * u];
+                S[2 * u + 1] = a.y + B[2 * u + 1];
+            }
+            const double st = small_stat<D>(S, DD, bal.g, ccr, bal.cst);
+            const bool keep = valid && (uint64_t)__double_as_longlong(st) <= hbits;
+            const unsigned m = __ballot_sync(FRR_FULL, keep);
+            if (m) {
+                unsigned long long at = 0;
+                if (lane == 0) at = atomicAdd(fcount, (unsigned long long)__popc(m));
+                at = __shfl_sync(FRR_FULL, at, 0) + __popc(m & ((1u << lane) - 1u));
+                if (keep && at < (unsigned long long)cap) {
+                    fidx[at] = r;
+                    fval[at] = st;
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------ exact rows, thread per rank
 // n <= 64: each thread unranks its rank into a unit mask (the combinadic
 // walk of k_exact_small), a warp stages its 32 rows in shared memory and
@@ -905,6 +977,19 @@ int launch_subset_sums(const frr_balance_t* bal, int na, const int32_t* lb, int6
     return frr_check_launch("k_subset_sums");
 }
 
+template <int D, int DD>
+int launch_tiled(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, const int64_t* tiles,
+                 int64_t ntiles, const int32_t* g_a, const int64_t* g_base, int64_t rank_lo, int64_t rank_hi,
+                 const SplitFilter& f, void* stream) {
+    auto kern = k_exact_tiled<D, DD>;
+    int rc = frr_prepare_kernel(kern, 0);
+    if (rc) return rc;
+    int grid = frr_persistent_grid(kern, kTileRows, 0, ntiles);
+    kern<<<grid, kTileRows, 0, frr_stream(stream)>>>(*bal, sa, sb, tiles, ntiles, g_a, g_base, rank_lo, rank_hi,
+                                                     f.hbits, f.cap, f.idx, f.val, f.count);
+    return frr_check_launch("k_exact_tiled");
+}
+
 int split_dispatch(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width, const int32_t* blk_a,
                    const int64_t* blk_off, const int64_t* blk_base, int64_t nblk, uint64_t rank_lo, int64_t count,
                    double* stats, const SplitFilter* f, int64_t stride, void* stream) {
@@ -1116,4 +1201,31 @@ extern "C" int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t*
     k_microbench_draws<<<grid, 256, 0, frr_stream(stream)>>>(per_thread, st, sink);
     if (total_draws_host) *total_draws_host = (int64_t)grid * 256 * per_thread;
     return frr_check_launch("k_microbench_draws");
+}
+
+extern "C" int frr_exact_tiled_filtered(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
+                                        const int64_t* tiles, int64_t ntiles, const int32_t* g_a,
+                                        const int64_t* g_base, uint64_t rank_lo, uint64_t rank_hi, uint64_t h_bits,
+                                        int64_t cap, int64_t* idx, double* vals, uint64_t* n_kept, void* stream) {
+    if (!bal || !n_kept || cap < 0 || (cap > 0 && (!idx || !vals)) || rank_hi < rank_lo)
+        return FRR_E_INVALID_DESIGN;
+    int rc = check_nt(bal->n, bal->t);
+    if (rc) return rc;
+    if (ntiles <= 0) return FRR_OK;
+    if (width != split_width(bal->d)) {
+        frr_set_error("frr_exact_tiled_filtered: width %d for d=%d", width, bal->d);
+        return FRR_E_UNSUPPORTED;
+    }
+    const SplitFilter f{h_bits, cap, idx, vals, reinterpret_cast<unsigned long long*>(n_kept)};
+    const int64_t lo = (int64_t)rank_lo, hi = (int64_t)rank_hi;
+#define FRR_TILED(W, DD) \
+    case DD: return launch_tiled<W, DD>(bal, sa, sb, tiles, ntiles, g_a, g_base, lo, hi, f, stream)
+    switch (bal->d) {
+        FRR_TILED(4, 1); FRR_TILED(4, 2); FRR_TILED(4, 3); FRR_TILED(4, 4);
+        FRR_TILED(6, 5); FRR_TILED(6, 6); FRR_TILED(8, 7); FRR_TILED(8, 8);
+        FRR_TILED(16, 9); FRR_TILED(16, 10); FRR_TILED(16, 11); FRR_TILED(16, 12);
+        FRR_TILED(16, 13); FRR_TILED(16, 14); FRR_TILED(16, 15); FRR_TILED(16, 16);
+        default: frr_set_error("frr_exact_tiled_filtered: d=%d", bal->d); return FRR_E_UNSUPPORTED;
+    }
+#undef FRR_TILED
 }

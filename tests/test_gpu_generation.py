@@ -384,3 +384,31 @@ def test_staged_to_host_pipelined(shape, dtype):
     for _ in range(2):
         got = NAT.to_host(t)
         assert got.dtype == t.cpu().numpy().dtype and np.array_equal(got, t.cpu().numpy())
+
+
+@pytest.mark.parametrize("n,t,d,lo,hi", [(24, 12, 5, 0, None), (27, 9, 3, 12_345, 3_000_001), (26, 13, 8, 777, None),
+                                         (30, 15, 16, 10**8, 10**8 + 2_000_003)])
+def test_tiled_filter_equals_rank_order_filter(monkeypatch, n, t, d, lo, hi):
+    """frr_exact_tiled_filtered keeps exactly the (rank, stat) pairs of
+    frr_exact_stats_split_filtered on a shard [lo, hi) that cuts blocks,
+    widths 4/6/8/16; n=24 also against the oracle's statistics."""
+    X = np.random.default_rng(n * d).standard_normal((n, d))
+    design = frr.DesignSpec(n, t, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    kern = frr.precompute_precision(X, "exact")._kernel
+    hi = math.comb(n, t) if hi is None else hi
+    count = hi - lo
+    samp = G._narrow_sample(kern, design, lo, max(1, count // 4096), 4096).cpu().numpy()
+    h = int(np.quantile(samp, 0.01, method="lower").view(np.uint64)) if samp.size else 0
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("FRR_EXACT_TILED", mode)
+        idx, val, nk = G._narrow_filter(kern, design, lo, count, h, count // 20 + 4096)
+        o = np.argsort(idx[:nk].cpu().numpy())
+        out[mode] = (idx[:nk].cpu().numpy()[o], val[:nk].cpu().numpy()[o], nk)
+    assert out["1"][2] == out["0"][2] > 0
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    if n == 24:
+        bal = O.balance_setup(X, O.precision(X, "exact"))
+        st = O.c_exact_stats(bal, t, 0, count)
+        want = np.flatnonzero(st.view(np.uint64) <= np.uint64(h))
+        assert np.array_equal(out["1"][0], want) and np.array_equal(out["1"][1], st[want])
