@@ -412,3 +412,14 @@ def test_tiled_filter_equals_rank_order_filter(monkeypatch, n, t, d, lo, hi):
         st = O.c_exact_stats(bal, t, 0, count)
         want = np.flatnonzero(st.view(np.uint64) <= np.uint64(h))
         assert np.array_equal(out["1"][0], want) and np.array_equal(out["1"][1], st[want])
+
+
+def test_c4_fused_pool_equals_unfused_full_size(monkeypatch):
+    """C4 at full size (2,333,606,220 ranks): the fused tiled path's pool is
+    the unfused path's (18.7 GB statistics array + select), which the
+    full-size parity run checked against the oracle (profiles/r01f_full_parity_c4.json)."""
+    X = np.random.default_rng(4).standard_normal((34, 5))
+    design = frr.DesignSpec(34, 17, accept_prob=1e-3, mode="exact", enumeration_cap=3 * 10**9)
+    fused, plain = _exact_pool_both(X, design, monkeypatch)
+    assert fused.n_accepted == 2_333_606
+    assert G.pools_equal(fused, plain) and np.array_equal(fused.assignments, plain.assignments)
