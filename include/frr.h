@@ -127,11 +127,11 @@ int frr_exact_stats_split_filtered(const frr_balance_t* bal, const int64_t* sa, 
                                    int64_t nblk, uint64_t rank_lo, int64_t count, uint64_t h_bits, int64_t cap,
                                    int64_t* idx, double* vals, uint64_t* n_kept, void* stream);
 /* frr_exact_stats_split_filtered reordered for reuse (same kept set, tile
- * order): tiles[i] = {sb_row0, j0 << 32 | nrows, g0, ng} pairs nrows <= 256
+ * order): tiles[i] = {sb_row0, j0 << 32 | nrows, g0, interior << 32 | ng} pairs nrows <= 256
  * consecutive upper subsets of one size s (SB rows sb_row0.., positions j0..
  * in their segment) with ng <= 256 blocks of that s (lower masks g_a[g0..],
  * base ranks g_base[g0..]); candidate (g, j) has rank g_base[g] + j and is
- * considered when rank_lo <= rank < rank_hi.  Host plan:
+ * considered when rank_lo <= rank < rank_hi (interior = 1: all of the tile is).  Host plan:
  * generation._tile_plan. */
 int frr_exact_tiled_filtered(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,
                              const int64_t* tiles, int64_t ntiles, const int32_t* g_a, const int64_t* g_base,

@@ -1,3 +1,4 @@
+#include <type_traits>
 // frr_gen.cu -- candidate generation, CUDA-core balance checks, regeneration
 // and the randomization-test kernels (sm_100a).
 //
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(256) k_exact_split(frr_balance_t bal, const in
 // base_g + j.  Every SB row is loaded once per tile instead of once per
 // candidate, so the kernel is bound by the fp64 epilogue, not by L2.  Only
 // the filtered output exists (ranks come out in tile order; the caller
-// sorts).  tiles[i] = {sb_row0, j0 << 32 | nrows, g0, ng}.
+// sorts).  tiles[i] = {sb_row0, j0 << 32 | nrows, g0, interior << 32 | ng}.
 constexpr int kTileRows = 256, kTileBlocks = 256;
 
 template <int D, int DD>  // DD = d, a compile-time constant: no per-column predicates in the epilogue
@@ -527,7 +528,8 @@ __global__ void __launch_bounds__(kTileRows) k_exact_tiled(frr_balance_t bal, co
     for (int u = 0; u < D; u++) ccr[u] = u < DD ? bal.cc[u] : 0.0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t sb_row0 = tiles[4 * tile], jn = tiles[4 * tile + 1], g0 = tiles[4 * tile + 2];
-        const int ng = (int)tiles[4 * tile + 3];
+        const int ng = (int)(tiles[4 * tile + 3] & 0xFFFFFFFF);
+        const bool interior = (tiles[4 * tile + 3] >> 32) != 0;  // every rank of the tile is in [lo, hi)
         const int nrows = (int)(jn & 0xFFFFFFFF);
         const int64_t j = (jn >> 32) + threadIdx.x;
         __syncthreads();  // previous tile's readers are done with sA
@@ -543,9 +545,10 @@ __global__ void __launch_bounds__(kTileRows) k_exact_tiled(frr_balance_t bal, co
             B[2 * u + 1] = v.y;
         }
         __syncthreads();
+        auto run = [&](auto inside) {
         for (int g = 0; g < ng; g++) {
             const int64_t r = sBase[g] + j;
-            const bool valid = row_ok && r >= rank_lo && r < rank_hi;
+            const bool valid = decltype(inside)::value ? row_ok : (row_ok && r >= rank_lo && r < rank_hi);
             const longlong2* ar = reinterpret_cast<const longlong2*>(sA + g * D);
             int64_t S[D];
 #pragma unroll
@@ -567,6 +570,9 @@ __global__ void __launch_bounds__(kTileRows) k_exact_tiled(frr_balance_t bal, co
                 }
             }
         }
+        };
+        if (interior) run(std::integral_constant<bool, true>{});
+        else run(std::integral_constant<bool, false>{});
     }
 }
 
