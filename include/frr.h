@@ -215,6 +215,15 @@ int frr_tau_counts(const double* a, const double* b, int64_t m, const double* ta
                    const double* rhs, int ntau, uint64_t* counts, void* stream);
 
 /* ---- diagnostics ------------------------------------------------------ */
+/* Thread-per-candidate generator (reverse-bitset Fisher-Yates) on its own:
+ * draws [draw_lo, draw_lo+count) -> CONTROL bitsets bits [count, ceil(n/32)]
+ * (bit e of word e/32 = unit e is control; NULL: not written) and an XOR
+ * checksum folded into *sink (NULL: none).  Same assignments as
+ * keys.py:138-159; used as the generator microbenchmark and its parity
+ * check (the fused pass-1 kernel runs the same device code). */
+int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count, int n, int t, uint32_t* bits,
+                 unsigned long long* sink, void* stream);
+
 /* D[128 x N] = A[128 x K] . B[N x K]^T (int8 row-major in, int32 out) on one
  * CTA through the same tcgen05 descriptor code as the fused kernel. */
 int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int N, int32_t* D, int variant,

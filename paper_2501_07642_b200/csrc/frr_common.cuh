@@ -346,6 +346,9 @@ __host__ __device__ __forceinline__ int frr_packed_unit(int w, int p) {
 // offset 4q + b).  The B operand rows are permuted to the same order.
 __host__ __device__ __forceinline__ int frr_kpos_bit(int r) { return 8 * (r & 3) + (r >> 2); }
 __host__ __device__ __forceinline__ int frr_k_unit(int kk) { return frr_packed_unit(kk >> 5, frr_kpos_bit(kk & 31)); }
+// the same K order over words in natural unit order (bit b of word w = unit
+// 32 w + b): the single-pass tensor-core kernel's tile rows
+__host__ __device__ __forceinline__ int frr_k_unit_nat(int kk) { return 32 * (kk >> 5) + frr_kpos_bit(kk & 31); }
 
 __device__ __forceinline__ uint32_t frr_pack_word(const uint16_t* lw, int w) {
     const uint4* src = reinterpret_cast<const uint4*>(lw + 32 * w);

@@ -3,9 +3,11 @@
 // Replaces generation.py:185-204 (_pass1_stats) = keys.py:177-208 feeding
 // balance.py:93-105 for mid-size d.  Per 128-candidate tile:
 //
-//   FY warps (26;   key -> assignment in a per-warp smem table (frr_warp_fy),
-//   fewer at large  packed to a bit row of the tile (never leaves the SM);
-//   n)              up to 3 bit-row tile buffers
+//   generator       GEN 1 (default): thread per candidate (frr_rev_fy, the
+//   warps           reverse-bitset Fisher-Yates), each warp builds 32 rows of
+//                   a tile buffer in place; GEN 0 (large n, whose bitsets do
+//                   not fit): warp per candidate (frr_warp_fy) into a smem
+//                   table, packed to the row.  Rows never leave the SM.
 //   tile warps (4)  expand bit rows to int8 0/1 A-operand K-chunks in the
 //                   tcgen05 K-major canonical layout; later the epilogue
 //   TMA warp        cp.async.bulk of the pre-tiled int8-limb B operand
@@ -21,6 +23,7 @@
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
+#include "frr_revfy.cuh"
 #include "frr_tc.cuh"
 
 namespace {
@@ -44,6 +47,17 @@ constexpr int NBITS = FRR_MMA_NBITS;  // max bit-row tile buffers between genera
 constexpr int A_STAGES = FRR_MMA_STAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
 constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: their tables share smem)
+// thread-per-candidate generators: RFY warps (4 per tile in flight, a
+// multiple of 4) building rows in place in RBITS tile buffers
+#ifndef FRR_MMA_RFY
+#define FRR_MMA_RFY 24
+#endif
+#ifndef FRR_MMA_RBITS
+#define FRR_MMA_RBITS 8
+#endif
+constexpr int RFY = FRR_MMA_RFY;
+constexpr int RBITS = FRR_MMA_RBITS;
+constexpr int MAXBITS = NBITS > RBITS ? NBITS : RBITS;
 // Wait-time accounting (debug builds only): per-slot clock64 sums read back
 // with frr_debug_waits().
 #ifndef FRR_MMA_TIMING
@@ -72,12 +86,14 @@ __device__ unsigned long long g_frr_waits[16];
 // copy and MMA warps, then the 4 tile warps at a multiple of 4 (warp % 4 is
 // their TMEM lane quadrant).  The scheduler favours higher warp ids, so the
 // latency-critical roles sit above the generators.
-constexpr int NTHREADS = (((NFY + 2 + 3) & ~3) + 4) * 32;  // launch bound: the largest layout
+constexpr int NTHREADS_MAX = ((((NFY > RFY ? NFY : RFY) + 2 + 3) & ~3) + 4) * 32;
+constexpr int NTHREADS = NTHREADS_MAX;  // launch bound: the largest layout
 constexpr int A_STAGE_BYTES = BM * KC;
 
 struct MmaShape {
     int n, t, d, L, dpad, npad, kpad, nkc, kw;  // kw: 32-bit words per bit row
     int nparts, part_n[2], part_off[2];
+    int gen;                                     // 1: thread-per-candidate generators, 0: warp per candidate
     int nfy, nbits;                              // generator warps, bit-row buffers
     int steps_smem;                              // step table in shared (1) or global memory
     int w_tma, w_mma, w_tile0, nwarps;           // warp roles
@@ -86,6 +102,12 @@ struct MmaShape {
 struct SmemPlan {
     size_t steps, tables, bits, a, b, bars, total;
 };
+
+// Tile buffer of 128 bit rows, kw words each, laid out [row / 32][word][row % 32]
+// (uint32): a thread-per-candidate generator owns one column of a 32-row
+// block and every access of a warp hits 32 distinct banks.  Bit b of word w
+// = unit 32 w + b is a CONTROL unit (padding beyond n reads as control).
+__host__ __device__ inline size_t bits_buf_bytes(int kw) { return (size_t)BM * kw * 4; }
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -97,11 +119,14 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     p.b = o;
     o += (size_t)B_STAGES * s.npad * KC;
     p.bits = o;
-    o += (size_t)s.nbits * BM * (s.kw + 4) * 4;
+    o += (size_t)s.nbits * bits_buf_bytes(s.kw);
     p.steps = o;
     if (s.steps_smem) o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
     p.tables = o;
-    o += (size_t)s.nfy * frr_table_len(s.n) * 2;
+    // GEN 0: one table per generator warp; GEN 1: one shared scratch table
+    // for the exact recomputation of flagged candidates (+ its lock word)
+    o += (size_t)(s.gen ? 1 : s.nfy) * frr_table_len(s.n) * 2;
+    if (s.gen) o = align_up(o + FRR_TABLE_SLACK, 16) + 16;
     o = align_up(o, 16);
     p.bars = o;
     o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
@@ -136,6 +161,16 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
     s.part_n[1] = s.npad - s.part_n[0];
     s.part_off[0] = 0;
     s.part_off[1] = s.part_n[0];
+    // Thread-per-candidate generators when their tile buffers fit: RFY / 4
+    // tiles being built plus two being consumed, at least 8 generator warps.
+    s.gen = 1;
+    s.steps_smem = 1;
+    for (int f = RFY; f >= 8; f -= 4) {
+        const int nb = f / 4 + 2 <= RBITS ? f / 4 + 2 : RBITS;
+        set_roles(s, f, nb);
+        if (smem_plan(s).total <= 227 * 1024) return s;
+    }
+    s.gen = 0;
     // Largest generator count with at least two bit buffers that fits shared
     // memory (tables are 2n bytes per generator, bit buffers n/8 per row);
     // large n falls back to one buffer and as few as 4 generators.
@@ -155,17 +190,17 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
 }
 
 // barrier slots
-constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = NBITS;
-constexpr int BAR_A_FULL = 2 * NBITS, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
+constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = MAXBITS;
+constexpr int BAR_A_FULL = 2 * MAXBITS, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
 constexpr int BAR_B_FULL = BAR_A_EMPTY + A_STAGES, BAR_B_EMPTY = BAR_B_FULL + B_STAGES;
 constexpr int BAR_TMEM_FULL = BAR_B_EMPTY + B_STAGES, BAR_TMEM_EMPTY = BAR_TMEM_FULL + 1;
 constexpr int N_BARS = BAR_TMEM_EMPTY + 1;
 static_assert(N_BARS <= 30, "barrier slots");
 
-// GS: step table in global memory (large n), else in shared memory
-// GS: step table in global memory (large n), else in shared memory.
-// FULL: NFY generator warps and NBITS bit buffers (compile-time constants).
-template <bool GS, bool FULL>
+// GEN 1: thread-per-candidate generators (step table in shared memory).
+// GEN 0, GS: step table in global memory (large n), else in shared memory.
+// FULL: the default generator/buffer counts as compile-time constants.
+template <bool GS, bool FULL, int GEN>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_mc_stats_mma(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out,
                    const StepC* __restrict__ gsteps) {
@@ -175,9 +210,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const MmaShape S = mma_shape(bal.n, bal.t, bal.d, bal.n_limbs);
     const SmemPlan P = smem_plan(S);
-    // FULL: the default layout (NFY generators, NBITS buffers) as compile-time
-    // constants -- the fast path; otherwise the shape's reduced layout
-    const int c_nfy = FULL ? NFY : S.nfy, c_nbits = FULL ? NBITS : S.nbits;
+    // FULL: the default layout (NFY / RFY generators, NBITS / RBITS buffers)
+    // as compile-time constants -- the fast path; otherwise the shape's
+    // reduced layout
+    const int c_nfy = FULL ? (GEN ? RFY : NFY) : S.nfy, c_nbits = FULL ? (GEN ? RBITS : NBITS) : S.nbits;
     const int c_w_tma = c_nfy, c_w_mma = c_nfy + 1, c_w_tile0 = (c_nfy + 2 + 3) & ~3;
     unsigned char* sA = smem + P.a;
     unsigned char* sB = smem + P.b;
@@ -186,10 +222,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    // GEN 1: lock of the shared fixup table (last 16 bytes before the barriers)
+    int* fix_lock = reinterpret_cast<int*>(smem + P.bars - 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
-    const int rowstride = S.kw + 4;  // words; +16 B breaks bank aliasing of rows
+    const size_t buf_words = (size_t)BM * S.kw;
 #if FRR_MMA_TIMING
     long long wacc[16] = {0};
     const long long tstart = clock64();
@@ -197,8 +235,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (!GS) frr_fill_steps(ssteps, S.n, S.t);
     if (threadIdx.x == 0) {
+        if (GEN) *fix_lock = 0;
         for (int b = 0; b < c_nbits; b++) {
-            mbar_init(&bars[BAR_BITS_FULL + b], c_nfy);
+            mbar_init(&bars[BAR_BITS_FULL + b], GEN ? 4 : c_nfy);
             mbar_init(&bars[BAR_BITS_EMPTY + b], 4);
         }
         for (int s = 0; s < A_STAGES; s++) {
@@ -223,25 +262,59 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp < c_nfy) {
-        // ===================================================== generators
+    if (GEN && warp < c_nfy) {
+        // ================================ thread-per-candidate generators
+        // warp g builds quadrant g % 4 (rows 32 q .. 32 q + 31) of the
+        // CTA's tiles g / 4, g / 4 + nfy / 4, ... in place in their buffers
+        const int q = warp & 3, kstep = c_nfy >> 2;
+        const uint32_t sst = smem_u32(ssteps);
+        for (int64_t k = warp >> 2;; k += kstep) {
+            const int64_t tile = blockIdx.x + k * gridDim.x;
+            if (tile >= ntiles) break;
+            const int buf = (int)(k % c_nbits);
+            TW(0, mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((k / c_nbits) & 1) ^ 1));
+            const uint32_t blk = smem_u32(sBits + (size_t)buf * buf_words + (size_t)q * S.kw * 32);
+            const uint64_t state = frr_derive_state(seed, lo + (uint64_t)(tile * BM + 32 * q + lane));
+            bool flag = false;
+            if (!(FRR_MMA_DEBUG & 1)) TW(11, flag = frr_rev_fy(state, S.t, sst, blk + 4u * lane, S.kw));
+            uint32_t fl = __ballot_sync(FRR_FULL, flag);
+            while (fl) {  // p ~ 1e-7 per candidate: exact recomputation in the shared scratch table
+                const int src = __ffs(fl) - 1;
+                fl &= fl - 1;
+                if (lane == 0)
+                    while (atomicCAS(fix_lock, 0, 1) != 0) __nanosleep(100);
+                __syncwarp();
+                frr_rev_fixup(__shfl_sync(FRR_FULL, state, src), S.n, S.t, ssteps, tables, blk + 4u * src, S.kw,
+                              lane);
+                if (lane == 0) atomicExch(fix_lock, 0);
+                __syncwarp();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[BAR_BITS_FULL + buf]);
+        }
+    } else if (!GEN && warp < c_nfy) {
+        // ===================================== warp-per-candidate generators
         const int fyw = warp;
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i % c_nbits;
             TW(0, mbar_wait_long(&bars[BAR_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1));
-            uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
+            uint32_t* tb = sBits + (size_t)buf * buf_words;
             for (int r = fyw; r < BM; r += c_nfy) {
                 const int64_t c = tile * BM + r;
-                uint32_t* row = tb + (size_t)r * rowstride;
+                uint32_t* row = tb + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
                 if (c < count && !(FRR_MMA_DEBUG & 1)) {
                     TW(11, frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, GS ? gsteps : ssteps,
                                        lw, lane));
-                    const int tw = frr_table_len(S.n) / 32;
-                    for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
+                    // control bits in natural unit order, one ballot per word
+                    for (int w = 0; w < S.kw; w++) {
+                        const int e = 32 * w + lane;
+                        const uint32_t word = __ballot_sync(FRR_FULL, e >= S.n || lw[e] == FRR_CTL);
+                        if (lane == (w & 31)) row[(size_t)w * 32] = word;
+                    }
                 } else {
-                    for (int w = lane; w < S.kw; w += 32) row[w] = 0;
+                    for (int w = lane; w < S.kw; w += 32) row[(size_t)w * 32] = ~0u;
                 }
                 __syncwarp();
             }
@@ -265,18 +338,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (lane == 0) mbar_arrive(&bars[BAR_BITS_EMPTY + buf]);
                 continue;
             }
-            const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
+            // row r: word w at [r / 32][w][r % 32]; control bits -> treated
+            const uint32_t* row = sBits + (size_t)buf * buf_words + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
                 const int s = astage % A_STAGES;
                 TW(2, mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1));
-                const uint32_t* src = row + kc * (KC / 32);
+                const uint32_t* src = row + (size_t)kc * (KC / 32) * 32;
                 uint32_t wv[KC / 32];
 #pragma unroll
-                for (int q = 0; q < KC / 32; q++) wv[q] = src[q];
+                for (int q = 0; q < KC / 32; q++) wv[q] = ~src[q * 32];
                 unsigned char* dst = sA + (size_t)s * A_STAGE_BYTES + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
                 for (int k16 = 0; k16 < KC / 16; k16++) {
-                    // bytes 4j..4j+3 of this slab: (w >> (4*half + j)) & 0x01010101 (frr_kpos_bit order)
+                    // bytes 4j..4j+3 of this slab: (w >> (4*half + j)) & 0x01010101
+                    // (K offset 4q + b <- bit 8b + q of the word: frr_k_unit_nat)
                     const uint32_t w = wv[k16 >> 1];
                     const int q0 = (k16 & 1) * 4;
                     uint4 o;
@@ -415,7 +490,7 @@ __global__ void k_prepare_limbs(const int64_t* __restrict__ zq, MmaShape S, int8
         int rem3 = rem2 % 128;
         int rr = rem3 / 16, kb = rem3 % 16;
         int kk = kc * KC + k16 * 16 + kb;  // K index
-        int k = frr_k_unit(kk);             // unit behind that K position
+        int k = frr_k_unit_nat(kk);         // unit behind that K position
         int nrow = n8 * 8 + rr;
         int l = nrow / S.dpad, j = nrow % S.dpad;
         int8_t v = 0;
@@ -589,9 +664,10 @@ int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64
     if (tc_layout(bal->n, bal->d, bal->n_limbs) == TC_NT) return frr_mc_stats_nt(bal, seed, lo, count, stats, stream);
     MmaShape S = mma_shape(bal->n, bal->t, bal->d, bal->n_limbs);
     SmemPlan P = smem_plan(S);
-    const bool full = S.nfy == NFY && S.nbits == NBITS;
-    const auto kern = S.steps_smem ? (full ? k_mc_stats_mma<false, true> : k_mc_stats_mma<false, false>)
-                                   : (full ? k_mc_stats_mma<true, true> : k_mc_stats_mma<true, false>);
+    const bool full = S.gen ? (S.nfy == RFY && S.nbits == RBITS) : (S.nfy == NFY && S.nbits == NBITS);
+    const auto kern = S.gen ? (full ? k_mc_stats_mma<false, true, 1> : k_mc_stats_mma<false, false, 1>)
+                      : S.steps_smem ? (full ? k_mc_stats_mma<false, true, 0> : k_mc_stats_mma<false, false, 0>)
+                                     : (full ? k_mc_stats_mma<true, true, 0> : k_mc_stats_mma<true, false, 0>);
     int rc = frr_prepare_kernel(kern, P.total);
     if (rc) return rc;
     int64_t ntiles = frr_cdiv(count, BM);

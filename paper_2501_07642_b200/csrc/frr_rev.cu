@@ -1,0 +1,105 @@
+// frr_rev.cu -- thread-per-candidate generator (frr_revfy.cuh) as a
+// stand-alone kernel: Monte Carlo draws -> packed control bitsets.
+//
+// Serves the generator microbenchmark (throughput of the bare key ->
+// assignment work, frr_microbench_revfy) and its GPU parity check against
+// the warp generator / the reference keys (frr_rev_bits).
+#include <cuda_runtime.h>
+
+#include "frr_common.cuh"
+#include "frr_launch.cuh"
+#include "frr_revfy.cuh"
+
+namespace {
+constexpr int kRevWarps = 16;
+
+struct RevPlan {
+    int kw, warps;
+    size_t steps_off, ws_off, fix_off, lock_off, total;
+};
+
+RevPlan rev_plan(int n, int t) {
+    RevPlan p;
+    p.kw = (n + 31) / 32;
+    p.warps = kRevWarps;
+    // fewer warps when the bitsets of 16 do not fit shared memory
+    while (p.warps > 1 && (size_t)p.warps * 32 * p.kw * 4 + (size_t)frr_steps_len(t) * sizeof(StepC) +
+                                  (size_t)frr_table_len(n) * 2 + FRR_TABLE_SLACK + 64 > 227 * 1024)
+        p.warps--;
+    size_t o = 0;
+    p.steps_off = o;
+    o += (size_t)frr_steps_len(t) * sizeof(StepC);
+    p.ws_off = o;
+    o += (size_t)p.warps * 32 * p.kw * 4;
+    p.fix_off = o;
+    o += (size_t)frr_table_len(n) * 2 + FRR_TABLE_SLACK;
+    o = (o + 15) & ~(size_t)15;
+    p.lock_off = o;
+    o += 16;
+    p.total = o;
+    return p;
+}
+
+// out: bits [count, kw] (control bit e of word e/32), optional; sink: XOR
+// of every candidate's words (optional; keeps the work alive in benchmarks)
+__global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, uint64_t lo, int64_t count, int n, int t,
+                                                             RevPlan P, uint32_t* __restrict__ out,
+                                                             unsigned long long* sink) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    StepC* steps = reinterpret_cast<StepC*>(smem + P.steps_off);
+    uint16_t* fix = reinterpret_cast<uint16_t*>(smem + P.fix_off);
+    int* lock = reinterpret_cast<int*>(smem + P.lock_off);
+    frr_fill_steps(steps, n, t);
+    if (threadIdx.x == 0) *lock = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sst = (uint32_t)__cvta_generic_to_shared(steps);
+    const uint32_t wsa0 = (uint32_t)__cvta_generic_to_shared(smem + P.ws_off) + (uint32_t)warp * 128u * P.kw;
+    const uint32_t wsa = wsa0 + 4u * lane;
+    uint32_t acc = 0;
+    const int64_t njobs = (count + 31) / 32;
+    for (int64_t job = (int64_t)blockIdx.x * P.warps + warp; job < njobs; job += (int64_t)gridDim.x * P.warps) {
+        const int64_t c = job * 32 + lane;
+        const uint64_t state = frr_derive_state(seed, lo + (uint64_t)c);
+        const bool flag = frr_rev_fy(state, t, sst, wsa, P.kw);
+        uint32_t fl = __ballot_sync(FRR_FULL, flag);
+        while (fl) {
+            const int src = __ffs(fl) - 1;
+            fl &= fl - 1;
+            if (lane == 0)
+                while (atomicCAS(lock, 0, 1) != 0) {
+                }
+            __syncwarp();
+            frr_rev_fixup(__shfl_sync(FRR_FULL, state, src), n, t, steps, fix, wsa0 + 4u * src, P.kw, lane);
+            if (lane == 0) atomicExch(lock, 0);
+            __syncwarp();
+        }
+        for (int w = 0; w < P.kw; w++) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsa + 128u * (uint32_t)w) : "memory");
+            acc ^= v * (uint32_t)(2 * w + 1);
+            if (out && c < count) out[(size_t)c * P.kw + w] = v;
+        }
+    }
+    if (sink && acc) atomicXor(sink, (unsigned long long)acc);
+}
+}  // namespace
+
+extern "C" int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count, int n, int t, uint32_t* bits,
+                            unsigned long long* sink, void* stream) {
+    if (n < 2 || t < 1 || t >= n || n > FRR_MAX_UNITS) {
+        frr_set_error("frr_rev_bits: need 0 < t < n <= %d", FRR_MAX_UNITS);
+        return FRR_E_INVALID_DESIGN;
+    }
+    if (count <= 0) return FRR_OK;
+    const RevPlan P = rev_plan(n, t);
+    if (P.total > 227 * 1024) {
+        frr_set_error("frr_rev_bits: n=%d too large for the shared bitsets", n);
+        return FRR_E_UNSUPPORTED;
+    }
+    int rc = frr_prepare_kernel(k_rev_bits, P.total);
+    if (rc) return rc;
+    const int grid = frr_persistent_grid(k_rev_bits, P.warps * 32, P.total, frr_cdiv(count, 32 * P.warps));
+    k_rev_bits<<<grid, P.warps * 32, P.total, frr_stream(stream)>>>(root_seed, draw_lo, count, n, t, P, bits, sink);
+    return frr_check_launch("k_rev_bits");
+}

@@ -1,0 +1,139 @@
+// frr_revfy.cuh -- thread-per-candidate key -> assignment generator
+// ("reverse bitset" Fisher-Yates), sm_100a.
+//
+// The reference draws r_j = j + u_j mod (n - j) for j = 0..t-1 and swaps
+// perm[j] <-> perm[r_j] (keys.py:146-158); the treated units are perm[0..t).
+// With perm_0 = identity, the final array is perm_t[x] = tau_0(tau_1(...
+// tau_{t-1}(x))) (tau_j the transposition (j r_j)), so the CONTROL set is
+// the image of the position set {t..n-1} under tau_0 o ... o tau_{t-1}:
+// start from the bitset B = {t..n-1} and apply the transpositions in
+// reverse order, j = t-1 down to 0.  Before reverse step j, bit j is still
+// 0 (steps > j only touch positions > j), so the swap is
+//
+//     bit = B[r_j];  B[r_j] = 0;  B[j] |= bit
+//
+// and the state is an n-bit set (128 B at n = 1000) instead of a 2n-byte
+// permutation: one candidate per thread, no last-writer table, no verify
+// loop, no chain walk, and the final B is already the packed control mask
+// the tensor-core operand is built from.
+//
+// The stream value of step j is mix64(state + (j+1) C) unless an earlier
+// step rejected (keys.py:150-154), which needs hi(u) == 0xFFFFFFFF
+// (p ~ 2^-32 per draw): the generator reports such candidates and the caller
+// recomputes them with the exact sequential rule (frr_warp_fy).
+#pragma once
+#include "frr_common.cuh"
+
+// Shared-memory layout of a warp's 32 bitsets: word w of lane l at
+// ws_base + (w * 32 + l) * 4 -- every lane in its own bank whatever word it
+// touches.  Bit b of word w <-> unit 32 w + b; 1 = control.
+#ifndef FRR_REV_JSIDE
+#define FRR_REV_JSIDE 0  // 0: shared atomic OR for the j-side bit, 1: load/or/store
+#endif
+
+// one step-constant record (b, c2, M) of the shared step table; pure
+// register function of its address for the compiler (the table is
+// read-only while generators run), so loads can be hoisted ahead of the
+// bitset traffic
+__device__ __forceinline__ StepC frr_lds_step(uint32_t a) {
+    uint32_t x, y, z, w;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
+    StepC s;
+    s.b = x;
+    s.c2 = y;
+    s.M = ((uint64_t)w << 32) | z;
+    return s;
+}
+
+// words [from, to) of this lane's bitset = all ones (positions >= t: the
+// initial set; padding beyond n stays control, its operand rows are zero)
+__device__ __forceinline__ void frr_rev_fill(uint32_t wsa, int from, int to) {
+    for (int w = from; w < to; w++) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wsa + 128u * (uint32_t)w), "r"(~0u) : "memory");
+}
+
+// Builds the control bitset of candidate `state` into this lane's column of
+// the warp's bitset block (wsa = shared address of word 0 of this lane).
+// kw words are written (kw >= ceil(n / 32)).  steps: shared address of the
+// step table (frr_fill_steps: steps k >= t are dummies with b = 1, d = 0).
+// Returns true when some stream value had hi == 0xFFFFFFFF (possible
+// rejection: the candidate must be recomputed exactly).
+__device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps, uint32_t wsa, int kw) {
+    const int wtop = (t - 1) >> 5;
+    frr_rev_fill(wsa, wtop + 1, kw);
+    uint32_t hmax = 0;
+    // zeros opaque to the compiler: the high words of frr_mod_step's 64-bit
+    // addends stay live instead of being re-zeroed every draw
+    uint32_t z0 = (uint32_t)t >> 31, z1 = (uint32_t)(t + 1) >> 31;
+    // x = state + (j + 1) C for the step j about to run
+    uint64_t x = state + (uint64_t)(32 * wtop + 33) * FRR_GOLDEN;
+    for (int W = wtop; W >= 0; W--) {
+        const uint32_t wa = wsa + 128u * (uint32_t)W;
+        // word W before its own steps: positions >= t set
+        const int lo = 32 * W;
+        const uint32_t init = t >= lo + 32 ? 0u : (~0u << (t - lo));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(init) : "memory");
+        const uint32_t sa = steps + 16u * (uint32_t)lo;
+#pragma unroll
+        for (int jb = 31; jb >= 0; jb--) {
+            x -= FRR_GOLDEN;
+            const StepC s = frr_lds_step(sa + 16u * (uint32_t)jb);
+            const uint64_t u = frr_mix64(x);
+            hmax = max(hmax, (uint32_t)(u >> 32));
+            // e = r - 32 W: r's word is W + e / 32
+            const uint32_t d = frr_mod_step(u, s, z0, z1);
+            const uint32_t e = (uint32_t)jb + d;
+            uint32_t ra;
+            asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}"
+                : "=r"(ra)
+                : "r"(e), "r"(wa));
+#if FRR_REV_JSIDE == 0
+            // r-side: read the word, clear bit r; j-side: OR the bit into
+            // word W (its bit jb is 0 until now) -- rotating the isolated bit
+            // r & 31 right by d lands it on jb.  Program order of one
+            // thread's shared accesses keeps the r == j and same-word cases
+            // right.
+            asm volatile(
+                "{\n\t.reg .u32 w, c, m, v;\n\t"
+                "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
+                "ld.shared.u32 w, [%0];\n\t"
+                "and.b32 c, w, m;\n\t"
+                "xor.b32 w, w, c;\n\t"
+                "st.shared.u32 [%0], w;\n\t"
+                "shf.r.wrap.b32 v, c, c, %3;\n\t"
+                "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
+                "r"(e), "r"(wa), "r"(d)
+                : "memory");
+#else
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t.reg .u32 w, c, m, v;\n\t"
+                "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
+                "ld.shared.u32 w, [%0];\n\t"
+                "and.b32 c, w, m;\n\t"
+                "setp.ne.u32 p, c, 0;\n\t"
+                "xor.b32 w, w, c;\n\t"
+                "st.shared.u32 [%0], w;\n\t"
+                "ld.shared.u32 v, [%2];\n\t"
+                "@p or.b32 v, v, %3;\n\t"
+                "st.shared.u32 [%2], v;\n\t}" ::"r"(ra),
+                "r"(e), "r"(wa), "n"(1u << jb)
+                : "memory");
+#endif
+        }
+    }
+    return hmax == 0xFFFFFFFFu;
+}
+
+// Exact recomputation of one lane's candidate (src_lane) of the warp with
+// the sequential-rule warp generator (frr_warp_fy, rejection included) in
+// the scratch table lw, then its control bits into that lane's bitset column.
+// All 32 lanes call it together.
+__device__ inline void frr_rev_fixup(uint64_t state, int n, int t, const StepC* steps, uint16_t* lw,
+                                     uint32_t wsa_src, int kw, int lane) {
+    frr_warp_fy(state, n, t, steps, lw, lane);
+    for (int w = 0; w < kw; w++) {
+        const int e = 32 * w + lane;
+        const uint32_t word = __ballot_sync(FRR_FULL, e >= n || lw[e] == FRR_CTL);
+        if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wsa_src + 128u * (uint32_t)w), "r"(word) : "memory");
+    }
+    __syncwarp();
+}
