@@ -20,6 +20,7 @@
 // S = W . Zq is exact in every limb (|acc| <= 128 n < 2^31), so the
 // statistic is bit-identical to the reference's float64 BLAS path.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
@@ -45,6 +46,13 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 constexpr int KC = FRR_MMA_KC;  // K bytes per pipeline stage
 constexpr int NBITS = FRR_MMA_NBITS;  // max bit-row tile buffers between generators and tile warps
 constexpr int A_STAGES = FRR_MMA_STAGES;
+// A operand in TMEM (tcgen05.st of the 0/1 bytes; the MMA reads A from TMEM)
+// whenever the accumulator leaves room for >= 2 K stages of KC / 4 columns
+#ifndef FRR_MMA_TMEM_A
+#define FRR_MMA_TMEM_A 0
+#endif
+constexpr int A_TSTAGES = 8;  // max TMEM A stages
+constexpr int A_SLOTS = A_STAGES > A_TSTAGES ? A_STAGES : A_TSTAGES;
 constexpr int B_STAGES = FRR_MMA_STAGES;
 constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: their tables share smem)
 // thread-per-candidate generators: RFY warps (4 per tile in flight, a
@@ -77,6 +85,10 @@ __device__ unsigned long long g_frr_waits[16];
         __VA_ARGS__;  \
     } while (0)
 #endif
+// epilogue limb recombination through 32-bit limb pairs (tc_limbs8_pairs)
+#ifndef FRR_MMA_PAIRS
+#define FRR_MMA_PAIRS 1
+#endif
 // timing experiments only (results invalid): 1 no Fisher-Yates, 4 no epilogue,
 // 8 generators only (tile, copy and MMA roles just recycle the bit buffers)
 #ifndef FRR_MMA_DEBUG
@@ -94,6 +106,7 @@ struct MmaShape {
     int n, t, d, L, dpad, npad, kpad, nkc, kw;  // kw: 32-bit words per bit row
     int nparts, part_n[2], part_off[2];
     int gen;                                     // 1: thread-per-candidate generators, 0: warp per candidate
+    int ta, nsta;                                // A in TMEM (columns [npad, npad + nsta KC/4)), A stages
     int nfy, nbits;                              // generator warps, bit-row buffers
     int steps_smem;                              // step table in shared (1) or global memory
     int w_tma, w_mma, w_tile0, nwarps;           // warp roles
@@ -115,7 +128,7 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     SmemPlan p;
     size_t o = 0;
     p.a = o;
-    o += (size_t)A_STAGES * A_STAGE_BYTES;
+    if (!s.ta) o += (size_t)A_STAGES * A_STAGE_BYTES;
     p.b = o;
     o += (size_t)B_STAGES * s.npad * KC;
     p.bits = o;
@@ -129,8 +142,8 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     if (s.gen) o = align_up(o + FRR_TABLE_SLACK, 16) + 16;
     o = align_up(o, 16);
     p.bars = o;
-    o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
-    static_assert(32 * 8 + 16 >= FRR_TABLE_SLACK, "table slack");
+    o += 48 * 8 + 16;  // barriers + TMEM slot: also the FRR_TABLE_SLACK after the tables
+    static_assert(48 * 8 + 16 >= FRR_TABLE_SLACK, "table slack");
     p.total = o + 1024;  // slack for base alignment
     return p;
 }
@@ -161,6 +174,8 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
     s.part_n[1] = s.npad - s.part_n[0];
     s.part_off[0] = 0;
     s.part_off[1] = s.part_n[0];
+    s.ta = FRR_MMA_TMEM_A && s.npad + 2 * (KC / 4) <= 512;
+    s.nsta = s.ta ? min(A_TSTAGES, (512 - s.npad) / (KC / 4)) : A_STAGES;
     // Thread-per-candidate generators when their tile buffers fit: RFY / 4
     // tiles being built plus two being consumed, at least 8 generator warps.
     s.gen = 1;
@@ -191,11 +206,11 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
 
 // barrier slots
 constexpr int BAR_BITS_FULL = 0, BAR_BITS_EMPTY = MAXBITS;
-constexpr int BAR_A_FULL = 2 * MAXBITS, BAR_A_EMPTY = BAR_A_FULL + A_STAGES;
-constexpr int BAR_B_FULL = BAR_A_EMPTY + A_STAGES, BAR_B_EMPTY = BAR_B_FULL + B_STAGES;
+constexpr int BAR_A_FULL = 2 * MAXBITS, BAR_A_EMPTY = BAR_A_FULL + A_SLOTS;
+constexpr int BAR_B_FULL = BAR_A_EMPTY + A_SLOTS, BAR_B_EMPTY = BAR_B_FULL + B_STAGES;
 constexpr int BAR_TMEM_FULL = BAR_B_EMPTY + B_STAGES, BAR_TMEM_EMPTY = BAR_TMEM_FULL + 1;
 constexpr int N_BARS = BAR_TMEM_EMPTY + 1;
-static_assert(N_BARS <= 30, "barrier slots");
+static_assert(N_BARS <= 46, "barrier slots");
 
 // GEN 1: thread-per-candidate generators (step table in shared memory).
 // GEN 0, GS: step table in global memory (large n), else in shared memory.
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     StepC* ssteps = reinterpret_cast<StepC*>(smem + P.steps);
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 46);
     // GEN 1: lock of the shared fixup table (last 16 bytes before the barriers)
     int* fix_lock = reinterpret_cast<int*>(smem + P.bars - 16);
 
@@ -240,7 +255,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&bars[BAR_BITS_FULL + b], GEN ? 4 : c_nfy);
             mbar_init(&bars[BAR_BITS_EMPTY + b], 4);
         }
-        for (int s = 0; s < A_STAGES; s++) {
+        for (int s = 0; s < S.nsta; s++) {
             mbar_init(&bars[BAR_A_FULL + s], 4);
             mbar_init(&bars[BAR_A_EMPTY + s], 1);
         }
@@ -340,13 +355,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             // row r: word w at [r / 32][w][r % 32]; control bits -> treated
             const uint32_t* row = sBits + (size_t)buf * buf_words + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
+            // A stages in TMEM: this warp's lane quadrant, columns after the accumulator
+            const uint32_t a_tl = tmem_base + ((uint32_t)((warp - c_w_tile0) * 32) << 16) + (uint32_t)S.npad;
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
-                const int s = astage % A_STAGES;
-                TW(2, mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / A_STAGES) & 1) ^ 1));
+                const int s = astage % S.nsta;
+                TW(2, mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / S.nsta) & 1) ^ 1));
                 const uint32_t* src = row + (size_t)kc * (KC / 32) * 32;
                 uint32_t wv[KC / 32];
 #pragma unroll
                 for (int q = 0; q < KC / 32; q++) wv[q] = ~src[q * 32];
+                if (S.ta) {
+                    // register q of word w: K offsets 4q..4q+3 of its 32-group = column 8w + q
+                    tc_fence_after();
+                    uint32_t v[KC / 4];
+#pragma unroll
+                    for (int q = 0; q < KC / 4; q++) v[q] = (wv[q >> 3] >> (q & 7)) & 0x01010101u;
+                    tc_st16(a_tl + (uint32_t)(s * (KC / 4)), v);
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars[BAR_A_FULL + s]);
+                    continue;
+                }
                 unsigned char* dst = sA + (size_t)s * A_STAGE_BYTES + (r >> 3) * 128 + (r & 7) * 16;
 #pragma unroll
                 for (int k16 = 0; k16 < KC / 16; k16++) {
@@ -381,7 +411,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
                 if (jb >= d) break;
                 int64_t Sj[8];
+#if FRR_MMA_PAIRS
+                tc_limbs8_fast(tl + (uint32_t)jb, S.L, S.dpad, Sj);
+#else
                 tc_limbs8(tl + (uint32_t)jb, S.L, S.dpad, pair32, Sj);
+#endif
                 if (jb < full) {
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
@@ -435,11 +469,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 TW(5, mbar_wait_long(&bars[BAR_TMEM_EMPTY], (i & 1) ^ 1));
                 tc_fence_after();
                 for (int kc = 0; kc < S.nkc; kc++, stage++) {
-                    const int sa = stage % A_STAGES, sb = stage % B_STAGES;
-                    TW(6, mbar_wait(&bars[BAR_A_FULL + sa], (stage / A_STAGES) & 1));
+                    const int sa = stage % S.nsta, sb = stage % B_STAGES;
+                    TW(6, mbar_wait(&bars[BAR_A_FULL + sa], (stage / S.nsta) & 1));
                     TW(7, mbar_wait(&bars[BAR_B_FULL + sb], (stage / B_STAGES) & 1));
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + (size_t)sa * A_STAGE_BYTES);
+                    const uint32_t at = tmem_base + (uint32_t)S.npad + (uint32_t)(sa * (KC / 4));
                     const uint32_t b0 = smem_u32(sB + (size_t)sb * S.npad * KC);
 #pragma unroll
                     for (int ks = 0; ks < KC / 32; ks++) {
@@ -447,8 +482,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         for (int p = 0; p < S.nparts; p++) {
                             const uint64_t bd =
                                 umma_desc(b0 + ks * 2 * b_lbo + (uint32_t)(S.part_off[p] / 8) * 128, b_lbo, 128);
-                            tc_mma_i8(tmem_base + (uint32_t)S.part_off[p], ad, bd, idesc_i8(BM, S.part_n[p]),
-                                      (kc | ks) != 0);
+                            if (S.ta)
+                                tc_mma_i8_ts(tmem_base + (uint32_t)S.part_off[p], at + (uint32_t)(ks * 8), bd,
+                                             idesc_i8(BM, S.part_n[p]), (kc | ks) != 0);
+                            else
+                                tc_mma_i8(tmem_base + (uint32_t)S.part_off[p], ad, bd, idesc_i8(BM, S.part_n[p]),
+                                          (kc | ks) != 0);
                         }
                     }
                     tc_commit(&bars[BAR_A_EMPTY + sa]);
@@ -613,6 +652,11 @@ enum TcLayout { TC_NONE = 0, TC_SINGLE = 1, TC_NT = 2 };
 // without t (worst case t = n - 1) so the limb operand can be built once.
 TcLayout tc_layout(int n, int d, int L) {
     if (d <= 16 || L < 1 || L > 8 || n < 2 || n > FRR_MAX_UNITS) return TC_NONE;
+    static const int force_nt = [] {
+        const char* e = getenv("FRR_TC_FORCE_NT");
+        return e && *e == '1';
+    }();
+    if (force_nt && frr_nt_fits(n, d, L)) return TC_NT;
     MmaShape s = mma_shape(n, n - 1, d, L);
     if (s.npad <= 512 && s.nfy > 0) return TC_SINGLE;
     if (frr_nt_fits(n, d, L)) return TC_NT;

@@ -19,6 +19,7 @@
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
+#include "frr_revfy.cuh"
 #include "frr_tc.cuh"
 
 // Two instantiations: 256-byte K stages (half the barrier and commit traffic

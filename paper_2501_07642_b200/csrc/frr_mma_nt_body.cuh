@@ -14,6 +14,14 @@ constexpr int KC = FRR_NT_KC;  // K bytes per stage: this instantiation's (128 o
 #ifndef FRR_NT_NEXP
 #define FRR_NT_NEXP 8
 #endif
+// thread-per-candidate generators (frr_rev_fy): at most RFY warps (a
+// multiple of 4: one tile in flight per 4) and MAXB tile buffers
+#ifndef FRR_NT_RFY
+#define FRR_NT_RFY 16
+#endif
+#ifndef FRR_NT_MAXB
+#define FRR_NT_MAXB 8
+#endif
 // timing experiments only (results invalid): 1 no B loads, 2 no A stores,
 // 4 no epilogue work, 8 no Fisher-Yates
 #ifndef FRR_NT_DEBUG
@@ -42,6 +50,8 @@ __device__ unsigned long long g_nt_waits[16];
 // "stage consumed" barrier (a single tcgen05.commit) releases both halves.
 constexpr int NST = KC == 256 ? 2 : FRR_NT_ST;  // TMEM holds two 64-column A stages at KC = 256
 constexpr int NFY = FRR_NT_NFY;
+constexpr int RFY = FRR_NT_RFY;
+constexpr int MAXB = FRR_NT_MAXB;
 constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
 // Warp roles (the scheduler favours higher warp ids; the epilogue is the
 // measured bottleneck of this kernel, so it gets the highest ones).
@@ -69,19 +79,24 @@ __host__ __device__ constexpr int w_mma(int) { return W_EXP0 + NEXP + 1; }
 __host__ __device__ constexpr int w_epi0(int) { return 0; }
 __host__ __device__ constexpr int n_warps(int nfy) { return W_FY0 + nfy; }
 #endif
-constexpr int NWARPS = n_warps(NFY);
+constexpr int NWARPS = n_warps(NFY > RFY ? NFY : RFY);
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int DJ = 32;  // covariates per N-chunk
 constexpr int MAX_LEAVES = 1024;
 
 struct NtShape {
     int n, t, d, L, dpad, nch, nc, kpad, nkc, kw;
+    int gen;         // 1: thread-per-candidate generators (step table in shared memory), 0: warp per candidate
     int nfy, nbits;  // generator warps, bit-row buffers (fewer for large n)
 };
 
 struct NtPlan {
-    size_t a, b, bits, tables, starts, ncomb, bars, total;
+    size_t a, b, bits, steps, tables, starts, ncomb, bars, total;
 };
+
+// tile buffer: 128 bit rows of kw words, [row / 32][word][row % 32] (see
+// frr_mma.cu); bit b of word w = unit 32 w + b is a control unit
+__host__ __device__ inline size_t nt_buf_words(int kw) { return (size_t)BM * kw; }
 
 __host__ __device__ inline size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -92,9 +107,14 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     p.b = o;
     o += (size_t)NST * s.nc * KC;
     p.bits = o;
-    o += (size_t)s.nbits * BM * (s.kw + 4) * 4;
+    o += (size_t)s.nbits * nt_buf_words(s.kw) * 4;
+    p.steps = o;
+    if (s.gen) o += (size_t)frr_steps_len(s.t) * sizeof(StepC);
     p.tables = o;
-    o += (size_t)s.nfy * frr_table_len(s.n) * 2;
+    // GEN 0: a table per generator warp; GEN 1: one shared scratch table for
+    // the exact recomputation of flagged candidates, + its lock word
+    o += (size_t)(s.gen ? 1 : s.nfy) * frr_table_len(s.n) * 2;
+    if (s.gen) o = up(o + FRR_TABLE_SLACK, 16) + 16;
     o = up(o, 16);
     p.starts = o;
     o += up((size_t)(s.dpad / 8 + 31) / 32 * 4, 16);
@@ -120,8 +140,17 @@ __host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
     s.kpad = (n + KC - 1) / KC * KC;
     s.nkc = s.kpad / KC;
     s.kw = s.kpad / 32;
+    // thread-per-candidate generators when their tile buffers fit (nfy / 4
+    // tiles being built + two being consumed); else the warp generators with
     // the full layout (NFY generators, two bit buffers) when it fits, else
     // fewer generators / one buffer so that large n keeps the tensor cores
+    s.gen = 1;
+    for (int f = RFY; f >= 4; f -= 4) {
+        s.nfy = f;
+        s.nbits = f / 4 + 2 <= MAXB ? f / 4 + 2 : MAXB;
+        if (nt_plan(s).total <= 227 * 1024) return s;
+    }
+    s.gen = 0;
     for (int nb = 2; nb >= 1; nb--)
         for (int f = NFY; f >= 2; f--) {
             s.nfy = f;
@@ -134,7 +163,7 @@ __host__ __device__ inline NtShape nt_shape(int n, int t, int d, int L) {
 
 // one "stage full" barrier per ring slot, arrived on by the 8 expansion warps
 // and by the bulk copy (arrive + expect_tx)
-constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = 2, B_A_FULL = 4, B_B_FULL = B_A_FULL;
+constexpr int B_BITS_FULL = 0, B_BITS_EMPTY = MAXB, B_A_FULL = 2 * MAXB, B_B_FULL = B_A_FULL;
 constexpr int B_S_EMPTY = B_B_FULL + NST, B_TM_FULL = B_S_EMPTY + NST, B_TM_EMPTY = B_TM_FULL + 2;
 static_assert(B_TM_EMPTY + 2 <= 30, "barrier slots");
 
@@ -176,8 +205,15 @@ __device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity) {
 }
 
 // spin wait for the pipeline roles (suspend-hint and sleep variants measured no better)
+#ifndef FRR_NT_HW_LAZY
+#define FRR_NT_HW_LAZY 0
+#endif
 __device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
+#if FRR_NT_HW_LAZY
+    mbar_wait_lazy(b, parity);
+#else
     mbar_wait(b, parity);
+#endif
 }
 
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
@@ -185,8 +221,9 @@ __device__ __forceinline__ double comb8(const double (&r)[8]) {
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 }
 
-// FULL: NFY generator warps and two bit buffers as compile-time constants
-template <bool FULL>
+// FULL: the default generator and bit-buffer counts as compile-time
+// constants; GEN: thread-per-candidate (1) or warp-per-candidate (0) generators
+template <bool FULL, int GEN>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_mc_stats_nt(frr_balance_t bal, uint64_t seed, uint64_t lo, int64_t count, double* __restrict__ out,
                   const StepC* __restrict__ steps) {
@@ -196,28 +233,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const NtPlan P = nt_plan(S);
     unsigned char* sB = smem + P.b;
     uint32_t* sBits = reinterpret_cast<uint32_t*>(smem + P.bits);
+    StepC* ssteps = reinterpret_cast<StepC*>(smem + P.steps);
     uint16_t* tables = reinterpret_cast<uint16_t*>(smem + P.tables);
+    int* fix_lock = reinterpret_cast<int*>(smem + P.starts - 16);
     uint32_t* starts = reinterpret_cast<uint32_t*>(smem + P.starts);
     uint8_t* ncomb = smem + P.ncomb;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
-    const int rowstride = S.kw + 4;
+    const size_t buf_words = nt_buf_words(S.kw);
     const int nst = min(NST, (512 - 2 * S.nc) / (KC / 4));  // ring stages whose A fits in TMEM
-    const int c_nfy = FULL ? NFY : S.nfy, c_nbits = FULL ? 2 : S.nbits;
+    const int c_nfy = FULL ? (GEN ? RFY : NFY) : S.nfy, c_nbits = FULL ? (GEN ? RFY / 4 + 2 : 2) : S.nbits;
 #if FRR_NT_TIMING
     long long wacc[16] = {0};
     const long long tstart = clock64();
 #endif
 
     for (int i = threadIdx.x; i < (S.dpad / 8 + 31) / 32; i += blockDim.x) starts[i] = 0;
+    if (GEN) frr_fill_steps(ssteps, S.n, S.t);
     __syncthreads();
     if (threadIdx.x == 0) {
         int nleaf = 0;
         nt_build(0, S.d, starts, ncomb, nleaf);
+        if (GEN) *fix_lock = 0;
         for (int b = 0; b < c_nbits; b++) {
-            mbar_init(&bars[B_BITS_FULL + b], c_nfy);
+            mbar_init(&bars[B_BITS_FULL + b], GEN ? 4 : c_nfy);
             mbar_init(&bars[B_BITS_EMPTY + b], NEXP);
         }
         for (int s = 0; s < nst; s++) {
@@ -241,24 +282,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp >= W_FY0 && warp < W_FY0 + c_nfy) {
-        // ===================================================== generators
+    if (GEN && warp >= W_FY0 && warp < W_FY0 + c_nfy) {
+        // ================================ thread-per-candidate generators
+        // warp g builds quadrant g % 4 of the CTA's tiles g / 4, g / 4 +
+        // nfy / 4, ... in place in their buffers (frr_mma.cu)
+        const int fyw = warp - W_FY0, q = fyw & 3, kstep = c_nfy >> 2;
+        const uint32_t sst = smem_u32(ssteps);
+        for (int64_t k = fyw >> 2;; k += kstep) {
+            const int64_t tile = blockIdx.x + k * gridDim.x;
+            if (tile >= ntiles) break;
+            const int buf = (int)(k % c_nbits);
+            NTW(0, mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((k / c_nbits) & 1) ^ 1));
+            const uint32_t blk = smem_u32(sBits + (size_t)buf * buf_words + (size_t)q * S.kw * 32);
+            const uint64_t state = frr_derive_state(seed, lo + (uint64_t)(tile * BM + 32 * q + lane));
+            bool flag = false;
+            if (!(FRR_NT_DEBUG & 8)) flag = frr_rev_fy(state, S.t, sst, blk + 4u * lane, S.kw);
+            uint32_t fl = __ballot_sync(FRR_FULL, flag);
+            while (fl) {  // p ~ 1e-7 per candidate: exact recomputation in the shared scratch table
+                const int src = __ffs(fl) - 1;
+                fl &= fl - 1;
+                if (lane == 0)
+                    while (atomicCAS(fix_lock, 0, 1) != 0) __nanosleep(100);
+                __syncwarp();
+                frr_rev_fixup(__shfl_sync(FRR_FULL, state, src), S.n, S.t, ssteps, tables, blk + 4u * src, S.kw,
+                              lane);
+                if (lane == 0) atomicExch(fix_lock, 0);
+                __syncwarp();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[B_BITS_FULL + buf]);
+        }
+    } else if (!GEN && warp >= W_FY0 && warp < W_FY0 + c_nfy) {
+        // ===================================== warp-per-candidate generators
         const int fyw = warp - W_FY0;
         uint16_t* lw = tables + (size_t)fyw * frr_table_len(S.n);
-        const int tw = frr_table_len(S.n) / 32;
         int i = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i % c_nbits;
             NTW(0, mbar_wait_lazy(&bars[B_BITS_EMPTY + buf], ((i / c_nbits) & 1) ^ 1));
-            uint32_t* tb = sBits + (size_t)buf * BM * rowstride;
+            uint32_t* tb = sBits + (size_t)buf * buf_words;
             for (int r = fyw; r < BM; r += c_nfy) {
                 const int64_t c = tile * BM + r;
-                uint32_t* row = tb + (size_t)r * rowstride;
+                uint32_t* row = tb + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
                 if (c < count && !(FRR_NT_DEBUG & 8)) {
                     frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
-                    for (int w = lane; w < S.kw; w += 32) row[w] = w < tw ? frr_pack_word(lw, w) : 0u;
+                    // control bits in natural unit order, one ballot per word
+                    for (int w = 0; w < S.kw; w++) {
+                        const int e = 32 * w + lane;
+                        const uint32_t word = __ballot_sync(FRR_FULL, e >= S.n || lw[e] == FRR_CTL);
+                        if (lane == (w & 31)) row[(size_t)w * 32] = word;
+                    }
                 } else {
-                    for (int w = lane; w < S.kw; w += 32) row[w] = 0;
+                    for (int w = lane; w < S.kw; w += 32) row[(size_t)w * 32] = ~0u;
                 }
                 __syncwarp();
             }
@@ -279,7 +354,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, i++) {
             const int buf = i % c_nbits;
             NTW(1, mbar_wait_hw(&bars[B_BITS_FULL + buf], (i / c_nbits) & 1));
-            const uint32_t* row = sBits + ((size_t)buf * BM + r) * rowstride;
+            // row r: word w at [r / 32][w][r % 32]; control bits -> treated
+            const uint32_t* row = sBits + (size_t)buf * buf_words + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
             for (int c = 0; c < S.nch; c++) {
                 for (int kc = 0; kc < S.nkc; kc++) {
                     const int s = a_s;
@@ -289,11 +365,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         a_ph ^= 1;
                     }
                     tc_fence_after();
-                    const uint32_t* src = row + kc * (KC / 32) + part * WPT;
+                    const uint32_t* src = row + (size_t)(kc * (KC / 32) + part * WPT) * 32;
                     uint32_t v[WPT * 8];
 #pragma unroll
                     for (int q = 0; q < WPT; q++) {
-                        const uint32_t w = src[q], wh = w >> 4;
+                        const uint32_t w = ~src[q * 32], wh = w >> 4;
 #pragma unroll
                         for (int b = 0; b < 8; b++) {
                             // bit 8j+b of w lands in byte j of register b with weight
@@ -488,7 +564,7 @@ __global__ void k_prepare_limbs_nt(const int64_t* __restrict__ zq, NtShape S, in
         const int nrow = (rem2 / 128) * 8 + (rem2 % 128) / 16;
         const int kb = rem2 % 16;
         const int kk = kc * KC + k16 * 16 + kb;
-        const int k = frr_k_unit(kk);
+        const int k = frr_k_unit_nat(kk);
         const int l = nrow / DJ, j = c * DJ + nrow % DJ;
         int8_t v = 0;
         if (k < S.n && j < S.d && l < S.L) {
@@ -535,10 +611,11 @@ int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count
     NtShape S = nt_shape(bal->n, bal->t, bal->d, bal->n_limbs);
     NtPlan P = nt_plan(S);
     GlobalSteps gs;
-    int rc = gs.init(bal->n, bal->t, s);
+    int rc = S.gen ? 0 : gs.init(bal->n, bal->t, s);
     if (rc) return rc;
-    const bool full = S.nfy == NFY && S.nbits == 2;
-    const auto kern = full ? k_mc_stats_nt<true> : k_mc_stats_nt<false>;
+    const bool full = S.gen ? (S.nfy == RFY && S.nbits == RFY / 4 + 2) : (S.nfy == NFY && S.nbits == 2);
+    const auto kern = S.gen ? (full ? k_mc_stats_nt<true, 1> : k_mc_stats_nt<false, 1>)
+                            : (full ? k_mc_stats_nt<true, 0> : k_mc_stats_nt<false, 0>);
     if ((rc = frr_prepare_kernel(kern, P.total))) return rc;
     int64_t ntiles = frr_cdiv(count, BM);
     int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());

@@ -27,6 +27,9 @@
 // Shared-memory layout of a warp's 32 bitsets: word w of lane l at
 // ws_base + (w * 32 + l) * 4 -- every lane in its own bank whatever word it
 // touches.  Bit b of word w <-> unit 32 w + b; 1 = control.
+#ifndef FRR_REV_GROUP
+#define FRR_REV_GROUP 4  // draws computed ahead of their bit moves (divides 32)
+#endif
 #ifndef FRR_REV_JSIDE
 #define FRR_REV_JSIDE 0  // 0: shared atomic OR for the j-side bit, 1: load/or/store
 #endif
@@ -73,51 +76,63 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
         const uint32_t init = t >= lo + 32 ? 0u : (~0u << (t - lo));
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(init) : "memory");
         const uint32_t sa = steps + 16u * (uint32_t)lo;
+        // FRR_REV_GROUP draws computed ahead of their bit moves: independent
+        // register work the scheduler interleaves with the serial chain of
+        // shared-memory bit moves
 #pragma unroll
-        for (int jb = 31; jb >= 0; jb--) {
-            x -= FRR_GOLDEN;
-            const StepC s = frr_lds_step(sa + 16u * (uint32_t)jb);
-            const uint64_t u = frr_mix64(x);
-            hmax = max(hmax, (uint32_t)(u >> 32));
-            // e = r - 32 W: r's word is W + e / 32
-            const uint32_t d = frr_mod_step(u, s, z0, z1);
-            const uint32_t e = (uint32_t)jb + d;
-            uint32_t ra;
-            asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}"
-                : "=r"(ra)
-                : "r"(e), "r"(wa));
+        for (int jg = 31; jg >= 0; jg -= FRR_REV_GROUP) {
+            uint32_t dd[FRR_REV_GROUP];
+#pragma unroll
+            for (int i = 0; i < FRR_REV_GROUP; i++) {
+                x -= FRR_GOLDEN;
+                const StepC s = frr_lds_step(sa + 16u * (uint32_t)(jg - i));
+                const uint64_t u = frr_mix64(x);
+                hmax = max(hmax, (uint32_t)(u >> 32));
+                dd[i] = frr_mod_step(u, s, z0, z1);
+            }
+#pragma unroll
+            for (int i = 0; i < FRR_REV_GROUP; i++) {
+                const int jb = jg - i;
+                const uint32_t d = dd[i];
+                // e = r - 32 W: r's word is W + e / 32
+                const uint32_t e = (uint32_t)jb + d;
+                uint32_t ra;
+                asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}"
+                    : "=r"(ra)
+                    : "r"(e), "r"(wa));
 #if FRR_REV_JSIDE == 0
-            // r-side: read the word, clear bit r; j-side: OR the bit into
-            // word W (its bit jb is 0 until now) -- rotating the isolated bit
-            // r & 31 right by d lands it on jb.  Program order of one
-            // thread's shared accesses keeps the r == j and same-word cases
-            // right.
-            asm volatile(
-                "{\n\t.reg .u32 w, c, m, v;\n\t"
-                "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
-                "ld.shared.u32 w, [%0];\n\t"
-                "and.b32 c, w, m;\n\t"
-                "xor.b32 w, w, c;\n\t"
-                "st.shared.u32 [%0], w;\n\t"
-                "shf.r.wrap.b32 v, c, c, %3;\n\t"
-                "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
-                "r"(e), "r"(wa), "r"(d)
-                : "memory");
+                // r-side: read the word, clear bit r; j-side: OR the bit into
+                // word W (its bit jb is 0 until now) -- rotating the isolated
+                // bit r & 31 right by d lands it on jb.  Program order of one
+                // thread's shared accesses keeps the r == j and same-word
+                // cases right.
+                asm volatile(
+                    "{\n\t.reg .u32 w, c, m, v;\n\t"
+                    "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
+                    "ld.shared.u32 w, [%0];\n\t"
+                    "and.b32 c, w, m;\n\t"
+                    "xor.b32 w, w, c;\n\t"
+                    "st.shared.u32 [%0], w;\n\t"
+                    "shf.r.wrap.b32 v, c, c, %3;\n\t"
+                    "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
+                    "r"(e), "r"(wa), "r"(d)
+                    : "memory");
 #else
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t.reg .u32 w, c, m, v;\n\t"
-                "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
-                "ld.shared.u32 w, [%0];\n\t"
-                "and.b32 c, w, m;\n\t"
-                "setp.ne.u32 p, c, 0;\n\t"
-                "xor.b32 w, w, c;\n\t"
-                "st.shared.u32 [%0], w;\n\t"
-                "ld.shared.u32 v, [%2];\n\t"
-                "@p or.b32 v, v, %3;\n\t"
-                "st.shared.u32 [%2], v;\n\t}" ::"r"(ra),
-                "r"(e), "r"(wa), "n"(1u << jb)
-                : "memory");
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t.reg .u32 w, c, m, v;\n\t"
+                    "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
+                    "ld.shared.u32 w, [%0];\n\t"
+                    "and.b32 c, w, m;\n\t"
+                    "setp.ne.u32 p, c, 0;\n\t"
+                    "xor.b32 w, w, c;\n\t"
+                    "st.shared.u32 [%0], w;\n\t"
+                    "ld.shared.u32 v, [%2];\n\t"
+                    "@p or.b32 v, v, %3;\n\t"
+                    "st.shared.u32 [%2], v;\n\t}" ::"r"(ra),
+                    "r"(e), "r"(wa), "n"(1u << jb)
+                    : "memory");
 #endif
+            }
         }
     }
     return hmax == 0xFFFFFFFFu;

@@ -199,6 +199,37 @@ __device__ __forceinline__ void tc_limbs8(uint32_t base, int L, int stride, bool
     }
 }
 
+// The same S_j from 32-bit limb pairs p_i = acc_{2i+1} * 256 + acc_{2i}
+// (|acc| <= 128 t, so |p| < 2^31 whenever t < 65280): one TMEM round trip
+// per pair, then S = sum_i p_i 2^(16 i) with two int64 multiply-adds for
+// L = 6 (the C2 shape) instead of five.
+template <int L>
+__device__ __forceinline__ void tc_limbs8_pairs(uint32_t base, int stride, int64_t (&Sj)[8]) {
+    constexpr int NP = (L + 1) / 2;
+#pragma unroll
+    for (int i = NP - 1; i >= 0; i--) {
+        int32_t vh[8], vl[8];
+        const int lh = 2 * i + 1, ll = 2 * i;
+        if (lh < L) tc_ld8(base + (uint32_t)(lh * stride), vh);
+        tc_ld8(base + (uint32_t)(ll * stride), vl);
+        tc_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int32_t pi = lh < L ? vh[u] * 256 + vl[u] : vl[u];
+            Sj[u] = i == NP - 1 ? (int64_t)pi : Sj[u] * 65536 + (int64_t)pi;
+        }
+    }
+}
+
+__device__ __forceinline__ void tc_limbs8_fast(uint32_t base, int L, int stride, int64_t (&Sj)[8]) {
+    switch (L) {
+        case 6: tc_limbs8_pairs<6>(base, stride, Sj); break;
+        case 5: tc_limbs8_pairs<5>(base, stride, Sj); break;
+        case 7: tc_limbs8_pairs<7>(base, stride, Sj); break;
+        default: tc_limbs8(base, L, stride, false, Sj); break;
+    }
+}
+
 // instruction descriptor: kind::i8, D=s32, A=s8, B=s8, K-major both
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

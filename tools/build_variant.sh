@@ -19,7 +19,7 @@ else
 fi
 nvcc $FLAGS "$@" -c $srcf -o build/variants/${base}_$name.o 2> build/variants/${base}_$name.log || { cat build/variants/${base}_$name.log; exit 1; }
 objs=""
-for f in frr_abi frr_gen frr_select frr_mma frr_mma_nt; do
+for f in frr_abi frr_gen frr_select frr_mma frr_mma_nt frr_rev; do
   [ "$f" = "$base" ] && objs="$objs build/variants/${base}_$name.o" || objs="$objs build/$f.o"
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../../tools/variants/libfrr_$name.so $objs
