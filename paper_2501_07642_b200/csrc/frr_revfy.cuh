@@ -28,7 +28,10 @@
 // ws_base + (w * 32 + l) * 4 -- every lane in its own bank whatever word it
 // touches.  Bit b of word w <-> unit 32 w + b; 1 = control.
 #ifndef FRR_REV_GROUP
-#define FRR_REV_GROUP 4  // draws computed ahead of their bit moves (divides 32)
+#define FRR_REV_GROUP 8  // draws computed ahead of their bit moves (divides 32)
+#endif
+#ifndef FRR_REV_FETCH_AND
+#define FRR_REV_FETCH_AND 1  // 1: atom.and fetch-and-clear for the r-side bit
 #endif
 #ifndef FRR_REV_JSIDE
 #define FRR_REV_JSIDE 0  // 0: shared atomic OR for the j-side bit, 1: load/or/store
@@ -82,14 +85,20 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
 #pragma unroll
         for (int jg = 31; jg >= 0; jg -= FRR_REV_GROUP) {
             uint32_t dd[FRR_REV_GROUP];
+            uint32_t hh[FRR_REV_GROUP];
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
                 x -= FRR_GOLDEN;
                 const StepC s = frr_lds_step(sa + 16u * (uint32_t)(jg - i));
                 const uint64_t u = frr_mix64(x);
-                hmax = max(hmax, (uint32_t)(u >> 32));
+                hh[i] = (uint32_t)(u >> 32);
                 dd[i] = frr_mod_step(u, s, z0, z1);
             }
+            // a rejection needs hi(u) == 0xFFFFFFFF: running max, two draws per
+            // three-input max
+#pragma unroll
+            for (int i = 0; i + 1 < FRR_REV_GROUP; i += 2) hmax = max(hmax, max(hh[i], hh[i + 1]));
+            if (FRR_REV_GROUP & 1) hmax = max(hmax, hh[FRR_REV_GROUP - 1]);
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
                 const int jb = jg - i;
@@ -106,6 +115,18 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
                 // bit r & 31 right by d lands it on jb.  Program order of one
                 // thread's shared accesses keeps the r == j and same-word
                 // cases right.
+#if FRR_REV_FETCH_AND
+                // fetch-and-clear of bit r in one shared atomic (nm = ~m)
+                asm volatile(
+                    "{\n\t.reg .u32 w, c, nm, v;\n\t"
+                    "shf.l.wrap.b32 nm, %4, %4, %1;\n\t"
+                    "atom.shared.and.b32 w, [%0], nm;\n\t"
+                    "lop3.b32 c, w, nm, 0, 0x30;\n\t"  // w & ~nm
+                    "shf.r.wrap.b32 v, c, c, %3;\n\t"
+                    "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
+                    "r"(e), "r"(wa), "r"(d), "r"(0xFFFFFFFEu)
+                    : "memory");
+#else
                 asm volatile(
                     "{\n\t.reg .u32 w, c, m, v;\n\t"
                     "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
@@ -117,6 +138,7 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
                     "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
                     "r"(e), "r"(wa), "r"(d)
                     : "memory");
+#endif
 #else
                 asm volatile(
                     "{\n\t.reg .pred p;\n\t.reg .u32 w, c, m, v;\n\t"
