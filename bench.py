@@ -261,12 +261,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         _barrier(world)
         torch.cuda.synchronize()
+        launches0 = int(N.lib().frr_launch_count())
         t_start.record(stream)
         marks[0].record(stream)
         for i in range(args.steps):
             res = step(evs[i])
             marks[i + 1].record(stream)
         t_end.record(stream)
+        launches = int(N.lib().frr_launch_count()) - launches0  # libfrr kernels of the timed region
         torch.cuda.synchronize()
     gc.enable()
     if os.environ.get("FRR_BENCH_DEBUG"):
@@ -308,11 +310,6 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("k_mc_stats_mma_bytes_per_launch")
-    # libfrr kernels per step: pass 1 (1); sampled bound: init + 8 x (hist, pick)
-    # (17); narrowing: init + tile counts, scan, compact (4); radix select on the
-    # narrowed set + final compaction (17 + 3); + the (less, equal) count at
-    # world > 1 (cf. profiles/r01d_launch_shares.txt)
-    launches_per_step = 1 + 17 + 4 + 20 + (0 if world == 1 else 1)
     draw_peak = _draw_peak(N)
     issue = None
     ip = os.path.join(ROOT, "profiles", "issue.json")
@@ -342,7 +339,7 @@ def run_ours(args):
         "cpu_baseline": cb,
         "e2e": {"value": total / e2e_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "paper_2501_07642_b200.monte_carlo_pool(X_host, design)"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "accepted_per_step": k,
     }
@@ -365,6 +362,28 @@ def _draw_peak(N):
     return best
 
 
+def _self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N
+    ranks (one process per GPU, NCCL) through torch.distributed.run."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init log (communicator size per rank)
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -373,6 +392,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(_self_launch(args))
+    if world and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -15,8 +15,9 @@
  *     (a cudaStream_t passed as void*; NULL = legacy default stream).
  *   - Return value: FRR_OK (0) or an error code mirroring fastrr.errors
  *     (errors.py:9-88); frr_last_error() gives a thread-local message.
- *   - The library holds no global mutable state besides that message and
- *     per-device one-time kernel attributes; functions are reentrant.
+ *   - The library holds no global mutable state besides that message,
+ *     per-device one-time kernel attributes and a launch counter; functions
+ *     are reentrant.
  *   - n_units <= FRR_MAX_UNITS (uint16 positions in the generators).
  */
 #ifndef FRR_H
@@ -62,6 +63,9 @@ typedef struct frr_balance {
 
 int frr_abi_version(void);
 const char* frr_last_error(void);
+/* Process-wide number of libfrr kernel launches so far (all threads,
+ * devices and streams); a diagnostic counter, the only other global state. */
+unsigned long long frr_launch_count(void);
 /* number of SMs / compute capability of the current device */
 int frr_device_info(int* sm_count, int* cc_major, int* cc_minor);
 

@@ -87,7 +87,11 @@ class LocalComm:
 
 
 class TorchComm:
-    """torch.distributed collectives (NCCL for CUDA tensors, gloo on CPU)."""
+    """torch.distributed collectives: NCCL for CUDA tensors (the GPU path).
+
+    Under a gloo group (no CUDA collectives) CUDA tensors are staged through
+    host memory -- e.g. several ranks sharing one GPU for testing, or a
+    debugging run without NCCL; the results are the same, only slower."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -96,12 +100,23 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.stage = dist.get_backend(group) == "gloo"
 
     def all_reduce_(self, t):
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, group=self.group)
         return t
 
     def all_gather(self, t):
+        if self.stage and t.is_cuda:
+            h = t.contiguous().cpu()
+            out = [h.new_empty(h.shape) for _ in range(self.world)]
+            self.dist.all_gather(out, h, group=self.group)
+            return [o.to(t.device) for o in out]
         out = [t.new_empty(t.shape) for _ in range(self.world)]
         self.dist.all_gather(out, t.contiguous(), group=self.group)
         return out

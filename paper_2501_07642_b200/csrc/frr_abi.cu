@@ -1,4 +1,5 @@
 // frr_abi.cu -- error state and device helpers shared by the C-ABI.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 
@@ -21,6 +22,17 @@ int frr_check_launch(const char* what) {
     }
     return FRR_OK;
 }
+
+// process-wide count of libfrr kernel launches (diagnostic: bench.py reports
+// the launches of its timed region from it)
+static std::atomic<unsigned long long> g_launches{0};
+
+int frr_launched(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return frr_check_launch(what);
+}
+
+extern "C" unsigned long long frr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int frr_abi_version(void) { return FRR_ABI_VERSION; }
 

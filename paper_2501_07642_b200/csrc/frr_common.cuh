@@ -16,6 +16,8 @@
 // ---------------------------------------------------------------- error state
 void frr_set_error(const char* fmt, ...);
 int frr_check_launch(const char* what);
+// frr_check_launch after a kernel launch, counted by frr_launch_count()
+int frr_launched(const char* what);
 
 // -------------------------------------------------------------- splitmix64
 // keys.py:99-104

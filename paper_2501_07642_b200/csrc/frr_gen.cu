@@ -888,7 +888,7 @@ int launch_planned(const char* what, KS ks, KG kg, const WarpPlan& P, int n, int
         ks<<<grid, threads, P.smem, s>>>(args..., (const StepC*)nullptr);
     }
     (void)keys;
-    return frr_check_launch(what);
+    return frr_launched(what);
 }
 
 template <int SRC>
@@ -933,7 +933,7 @@ int launch_exact_small(const frr_balance_t* bal, uint64_t rank_lo, int64_t count
     if (rc) return rc;
     int grid = frr_persistent_grid(kern, kThreads, smem, frr_cdiv(count, (int64_t)kWarps * 32 * kRun));
     kern<<<grid, kThreads, smem, frr_stream(stream)>>>(*bal, rank_lo, count, out);
-    return frr_check_launch("k_exact_small");
+    return frr_launched("k_exact_small");
 }
 
 template <int SRC>
@@ -972,7 +972,7 @@ int launch_split(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb,
     const SplitFilter& F = f ? *f : z;
     kern<<<grid, 256, 0, frr_stream(stream)>>>(*bal, sa, sb, blk_a, blk_off, blk_base, nblk, rank_lo, count, out,
                                                F.hbits, F.cap, F.idx, F.val, F.count, stride);
-    return frr_check_launch(f ? "k_exact_split<filtered>" : "k_exact_split");
+    return frr_launched(f ? "k_exact_split<filtered>" : "k_exact_split");
 }
 
 template <int D>
@@ -980,7 +980,7 @@ int launch_subset_sums(const frr_balance_t* bal, int na, const int32_t* lb, int6
     const int64_t tot = (1ll << na) + (1ll << (bal->n - na));
     k_subset_sums<D><<<(int)std::min<int64_t>(frr_cdiv(tot, 256), 4096), 256, 0, frr_stream(stream)>>>(
         bal->zq, bal->n, bal->d, na, lb, sa, sb);
-    return frr_check_launch("k_subset_sums");
+    return frr_launched("k_subset_sums");
 }
 
 template <int D, int DD>
@@ -993,7 +993,7 @@ int launch_tiled(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb,
     int grid = frr_persistent_grid(kern, kTileRows, 0, ntiles);
     kern<<<grid, kTileRows, 0, frr_stream(stream)>>>(*bal, sa, sb, tiles, ntiles, g_a, g_base, rank_lo, rank_hi,
                                                      f.hbits, f.cap, f.idx, f.val, f.count);
-    return frr_check_launch("k_exact_tiled");
+    return frr_launched("k_exact_tiled");
 }
 
 int split_dispatch(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width, const int32_t* blk_a,
@@ -1140,7 +1140,7 @@ extern "C" int frr_regen_exact(const uint64_t* ranks, int64_t m, int n, int t, i
         if (rc) return rc;
         int grid = frr_persistent_grid(k_exact_rows_small, kRowsThreads, smem, frr_cdiv(m, (int64_t)kRowsThreads));
         k_exact_rows_small<<<grid, kRowsThreads, smem, frr_stream(stream)>>>(ranks, m, n, t, rows);
-        return frr_check_launch("k_exact_rows_small");
+        return frr_launched("k_exact_rows_small");
     }
     return launch_regen<SRC_RANKS>(0, ranks, m, n, t, rows, bits, stream);
 }
@@ -1172,7 +1172,7 @@ extern "C" int frr_tau_counts(const double* a, const double* b, int64_t m, const
     per_tile = std::min<int64_t>(per_tile, frr_cdiv(m, 256));
     dim3 grid((unsigned)per_tile, (unsigned)tiles);
     k_tau_counts<<<grid, 256, 0, s>>>(a, b, m, taus, rhs, ntau, reinterpret_cast<unsigned long long*>(counts));
-    return frr_check_launch("k_tau_counts");
+    return frr_launched("k_tau_counts");
 }
 
 // ------------------------------------------------------------ diagnostics
@@ -1206,7 +1206,7 @@ extern "C" int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t*
     const StepC st = frr_make_step(1000, 257);
     k_microbench_draws<<<grid, 256, 0, frr_stream(stream)>>>(per_thread, st, sink);
     if (total_draws_host) *total_draws_host = (int64_t)grid * 256 * per_thread;
-    return frr_check_launch("k_microbench_draws");
+    return frr_launched("k_microbench_draws");
 }
 
 extern "C" int frr_exact_tiled_filtered(const frr_balance_t* bal, const int64_t* sa, const int64_t* sb, int width,

@@ -61,7 +61,7 @@ struct GlobalSteps {
         if (cudaMallocAsync((void**)&p, (size_t)frr_steps_len(t) * sizeof(StepC), s) != cudaSuccess)
             return frr_check_launch("cudaMallocAsync(steps)");
         k_fill_steps_global<<<std::max(1, frr_steps_len(t) / 256), 256, 0, s>>>(p, n, t);
-        return frr_check_launch("k_fill_steps_global");
+        return frr_launched("k_fill_steps_global");
     }
     ~GlobalSteps() {
         if (p) cudaFreeAsync(p, s);

@@ -699,7 +699,7 @@ extern "C" int frr_prepare_limbs(const int64_t* zq, int n, int d, int n_limbs, i
     int64_t total = (int64_t)S.kpad * S.npad;
     int grid = (int)std::min<int64_t>(frr_cdiv(total, 256), (int64_t)frr_num_sms() * 16);
     k_prepare_limbs<<<grid, 256, 0, s>>>(zq, S, limbs, overflow_dev);
-    return frr_check_launch("k_prepare_limbs");
+    return frr_launched("k_prepare_limbs");
 }
 
 int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats,
@@ -719,7 +719,7 @@ int frr_mc_stats_mma(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64
     GlobalSteps gs;
     if (!S.steps_smem && (rc = gs.init(bal->n, bal->t, frr_stream(stream)))) return rc;
     kern<<<grid, S.nwarps * 32, P.total, frr_stream(stream)>>>(*bal, seed, lo, count, stats, gs.p);
-    return frr_check_launch("k_mc_stats_mma");
+    return frr_launched("k_mc_stats_mma");
 }
 
 extern "C" int frr_mc_stats_tc(const frr_balance_t* bal, uint64_t root_seed, uint64_t draw_lo, int64_t count,
@@ -741,7 +741,7 @@ extern "C" int frr_selftest_mma_i8(const int8_t* A, const int8_t* B, int K, int 
     int rc = frr_prepare_kernel(k_selftest_mma, smem);
     if (rc) return rc;
     k_selftest_mma<<<1, 128, smem, frr_stream(stream)>>>(A, B, K, N, D, variant);
-    return frr_check_launch("k_selftest_mma");
+    return frr_launched("k_selftest_mma");
 }
 
 // ---------------------------------------------------- tensor-pipe ceiling
@@ -827,7 +827,7 @@ extern "C" int frr_microbench_mma_i8(int N, int a_tmem, int64_t iters, int64_t* 
     const int grid = frr_num_sms();
     k_microbench_mma<<<grid, 128, smem, frr_stream(stream)>>>(N, a_tmem, iters);
     if (ops_host) *ops_host = (int64_t)grid * iters * 4 * 2 * BM * N * 32;
-    return frr_check_launch("k_microbench_mma");
+    return frr_launched("k_microbench_mma");
 }
 
 #if FRR_MMA_TIMING

@@ -602,7 +602,7 @@ int prepare_limbs(const int64_t* zq, int n, int d, int L, int8_t* limbs, int32_t
     int64_t total = (int64_t)limbs_bytes(n, d, L);
     int grid = (int)std::min<int64_t>(frr_cdiv(total, 256), (int64_t)frr_num_sms() * 16);
     k_prepare_limbs_nt<<<grid, 256, 0, s>>>(zq, S, limbs, overflow);
-    return frr_check_launch("k_prepare_limbs_nt");
+    return frr_launched("k_prepare_limbs_nt");
 }
 
 int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count, double* stats, void* stream) {
@@ -620,7 +620,7 @@ int mc_stats(const frr_balance_t* bal, uint64_t seed, uint64_t lo, int64_t count
     int64_t ntiles = frr_cdiv(count, BM);
     int grid = (int)std::min<int64_t>(ntiles, frr_num_sms());
     kern<<<grid, n_warps(S.nfy) * 32, P.total, s>>>(*bal, seed, lo, count, stats, gs.p);
-    return frr_check_launch("k_mc_stats_nt");
+    return frr_launched("k_mc_stats_nt");
 }
 
 #if FRR_NT_TIMING

@@ -101,5 +101,5 @@ extern "C" int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count,
     if (rc) return rc;
     const int grid = frr_persistent_grid(k_rev_bits, P.warps * 32, P.total, frr_cdiv(count, 32 * P.warps));
     k_rev_bits<<<grid, P.warps * 32, P.total, frr_stream(stream)>>>(root_seed, draw_lo, count, n, t, P, bits, sink);
-    return frr_check_launch("k_rev_bits");
+    return frr_launched("k_rev_bits");
 }

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kCThreads) k_compact(const uint64_t* __restric
 
 extern "C" int frr_select_init(frr_select_state_t* st, int64_t k, void* stream) {
     k_init<<<1, 1, 0, frr_stream(stream)>>>(st, k);
-    return frr_check_launch("k_init");
+    return frr_launched("k_init");
 }
 
 extern "C" int frr_select_hist(const double* stats, int64_t m, const frr_select_state_t* st, int pass,
@@ -282,12 +282,12 @@ extern "C" int frr_select_hist(const double* stats, int64_t m, const frr_select_
     int grid = (int)std::min<int64_t>(frr_cdiv(m, kHistThreads), (int64_t)frr_num_sms() * 4);
     k_hist<<<grid, kHistThreads, 0, s>>>(reinterpret_cast<const uint64_t*>(stats), m, st, 56 - 8 * pass,
                                          reinterpret_cast<unsigned long long*>(hist));
-    return frr_check_launch("k_hist");
+    return frr_launched("k_hist");
 }
 
 extern "C" int frr_select_pick(const uint64_t* hist, frr_select_state_t* st, int pass, void* stream) {
     k_pick<<<1, 32, 0, frr_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(hist), st, 56 - 8 * pass);
-    return frr_check_launch("k_pick");
+    return frr_launched("k_pick");
 }
 
 extern "C" int frr_select_count(const double* stats, int64_t m, const frr_select_state_t* st, int64_t* counts,
@@ -298,7 +298,7 @@ extern "C" int frr_select_count(const double* stats, int64_t m, const frr_select
     int grid = (int)std::min<int64_t>(frr_cdiv(m, 256), (int64_t)frr_num_sms() * 8);
     k_count<<<grid, 256, 0, s>>>(reinterpret_cast<const uint64_t*>(stats), m, st,
                                  reinterpret_cast<unsigned long long*>(counts));
-    return frr_check_launch("k_count");
+    return frr_launched("k_count");
 }
 
 extern "C" size_t frr_select_workspace_bytes(int64_t m) {
@@ -325,11 +325,11 @@ extern "C" int frr_select_compact_capped(const double* stats, int64_t m, int64_t
     int64_t* ws = reinterpret_cast<int64_t*>(workspace);
     const uint64_t* bits = reinterpret_cast<const uint64_t*>(stats);
     k_tile_counts<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, st, ws);
-    int rc = frr_check_launch("k_tile_counts");
+    int rc = frr_launched("k_tile_counts");
     if (rc) return rc;
     k_tile_scan<<<1, 1024, 0, s>>>(ws, ntiles, tie_quota, n_out);
-    if ((rc = frr_check_launch("k_tile_scan"))) return rc;
+    if ((rc = frr_launched("k_tile_scan"))) return rc;
     k_compact<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, index_base, st, tie_quota, ws, cap, idx_out,
                                                      stat_out);
-    return frr_check_launch("k_compact");
+    return frr_launched("k_compact");
 }

@@ -93,7 +93,13 @@ def _pack_bits(w: np.ndarray) -> np.ndarray:
 
 
 class _PoolStats:
-    """Device a, b (+ membership) of a pool for outcome y and observed w."""
+    """Device a, b (+ membership) of a pool for outcome y and observed w.
+
+    Under torch.distributed (world > 1) every rank computes a and b for its
+    contiguous shard of the pool only; the integer counts of p(tau) are
+    all-reduced (SURVEY section 8 e), and the full a -- needed only for
+    stat_distribution and np.std in the fiducial interval -- is gathered in
+    rank order on first use."""
 
     def __init__(self, pool: RandomizationPool, obs_w: np.ndarray, y: np.ndarray):
         torch = N.torch_mod()
@@ -104,33 +110,29 @@ class _PoolStats:
         y_dev = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(dev)
         obs_dev = torch.from_numpy(_pack_bits(obs_w).view(np.int32)).to(dev)
         match = torch.zeros(1, dtype=torch.int32, device=dev)
-        comm = default_comm()
+        self.comm = comm = default_comm()
+        lo, hi = self.m * comm.rank // comm.world, self.m * (comm.rank + 1) // comm.world
+        a = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+        b = torch.empty(hi - lo, dtype=torch.float64, device=dev)
         if pool.assignments is not None:
-            rows = pool.assignments
-            lo, hi = 0, self.m
-            if comm.world > 1:
-                lo, hi = self.m * comm.rank // comm.world, self.m * (comm.rank + 1) // comm.world
-            rows_dev = torch.from_numpy(np.ascontiguousarray(rows[lo:hi], dtype=np.int8)).to(dev)
-            a = torch.empty(hi - lo, dtype=torch.float64, device=dev)
-            b = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+            rows_dev = torch.from_numpy(np.ascontiguousarray(pool.assignments[lo:hi], dtype=np.int8)).to(dev)
             if hi > lo:
                 N.call("frr_dim_rows", N.ptr(rows_dev), hi - lo, n, t, N.ptr(y_dev), N.ptr(obs_dev), N.ptr(a),
                        N.ptr(b), N.ptr(match), N.stream_ptr())
         else:
             if pool.keys is None:
-                raise EmptyPoolError("pool has neither keys nor assignments")
-            lo, hi = 0, self.m
-            if comm.world > 1:
-                lo, hi = self.m * comm.rank // comm.world, self.m * (comm.rank + 1) // comm.world
+                # the reference's pool_assignment_matrix -> regenerate_assignments
+                # raises this for a pool without keys (generation.py:349-352)
+                raise InvalidDesignError(
+                    "pool stores no keys; exact-mode pools carry explicit assignments instead")
             draws = keymod.to_device_u64(np.ascontiguousarray(pool.keys[lo:hi, 1], dtype=np.uint64))
-            a = torch.empty(hi - lo, dtype=torch.float64, device=dev)
-            b = torch.empty(hi - lo, dtype=torch.float64, device=dev)
             if hi > lo:
                 N.call("frr_dim_mc", int(d.root_seed) & keymod.MASK64, N.ptr(draws), hi - lo, n, t, N.ptr(y_dev),
                        N.ptr(obs_dev), N.ptr(a), N.ptr(b), N.ptr(match), N.stream_ptr())
         if comm.world > 1:
-            a, b, match = self._gather(comm, a, b, match)
-        self.a, self.b = a, b
+            comm.all_reduce_(match)
+        self.a_local, self.b_local = a, b
+        self._a_full = a if comm.world == 1 else None
         self.in_pool = bool(int(match.sum().item()) != 0)
         # observed statistic through the same reduction (inference.py:124, 174-177)
         t_obs = int(obs_w.sum())
@@ -141,29 +143,40 @@ class _PoolStats:
         tau_obs, b_obs = ab.cpu().tolist()
         self.tau_obs, self.b_obs = float(tau_obs), float(b_obs)
 
+    @property
+    def a(self):
+        """The whole pool's a in pool order (gathered across ranks once)."""
+        if self._a_full is None:
+            self._a_full = self._gather(self.comm, self.a_local)
+        return self._a_full
+
     @staticmethod
-    def _gather(comm, a, b, match):
+    def _gather(comm, a):
         torch = N.torch_mod()
         n_local = torch.tensor([a.shape[0]], dtype=torch.int64, device=a.device)
         sizes = [int(s) for s in torch.stack(comm.all_gather(n_local)).reshape(-1).tolist()]
         mx = max(1, max(sizes))
         pa = torch.zeros(mx, dtype=a.dtype, device=a.device)
-        pb = torch.zeros(mx, dtype=b.dtype, device=b.device)
         pa[: a.shape[0]] = a
-        pb[: b.shape[0]] = b
-        ga, gb = comm.all_gather(pa), comm.all_gather(pb)
-        comm.all_reduce_(match)
-        return (torch.cat([g[:s] for g, s in zip(ga, sizes)]), torch.cat([g[:s] for g, s in zip(gb, sizes)]), match)
+        ga = comm.all_gather(pa)
+        return torch.cat([g[:s] for g, s in zip(ga, sizes)])
 
     def counts(self, taus, rhs) -> np.ndarray:
-        """#{|a - tau b| >= rhs} for each (tau, rhs) pair, one launch."""
+        """#{|a - tau b| >= rhs} over the whole pool for each (tau, rhs) pair:
+        one launch on this rank's shard, then an int64 all-reduce."""
         torch = N.torch_mod()
         taus = np.ascontiguousarray(taus, dtype=np.float64)
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
-        tt = torch.from_numpy(np.concatenate([taus, rhs])).to(self.a.device)
-        out = torch.empty(taus.shape[0], dtype=torch.int64, device=self.a.device)
-        N.call("frr_tau_counts", N.ptr(self.a), N.ptr(self.b), self.m, N.ptr(tt[: taus.shape[0]]),
-               N.ptr(tt[taus.shape[0]:]), taus.shape[0], N.ptr(out), N.stream_ptr())
+        dev = self.a_local.device
+        tt = torch.from_numpy(np.concatenate([taus, rhs])).to(dev)
+        out = torch.zeros(taus.shape[0], dtype=torch.int64, device=dev)
+        m_local = int(self.a_local.shape[0])
+        if m_local:
+            N.call("frr_tau_counts", N.ptr(self.a_local), N.ptr(self.b_local), m_local,
+                   N.ptr(tt[: taus.shape[0]]), N.ptr(tt[taus.shape[0]:]), taus.shape[0], N.ptr(out),
+                   N.stream_ptr())
+        if self.comm.world > 1:
+            self.comm.all_reduce_(out)
         return out.cpu().numpy()
 
 
@@ -227,7 +240,7 @@ def _fi_from_stats(ps: _PoolStats, alpha: float) -> tuple[float, float]:
         rhs = [abs(tau_obs - tau * b_obs) for tau in taus]
         return ps.counts(taus, rhs).astype(np.float64) / m
 
-    half = 10.0 * float(np.std(ps.a.cpu().numpy()))
+    half = 10.0 * float(np.std(N.to_host(ps.a)))
     if not np.isfinite(half) or half == 0.0:
         half = max(1.0, abs(tau_obs))
     lo_g, hi_g = tau_obs - half, tau_obs + half

@@ -14,6 +14,7 @@ GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA product path)")
     config.addinivalue_line("markers", "slow: long-running parity check")
+    config.addinivalue_line("markers", "conformance: the reference's own test suite run against the drop-in")
 
 
 @pytest.fixture(scope="session")
