@@ -1,4 +1,3 @@
-#include <type_traits>
 // frr_gen.cu -- candidate generation, CUDA-core balance checks, regeneration
 // and the randomization-test kernels (sm_100a).
 //
@@ -9,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"

@@ -324,19 +324,32 @@ def test_fused_exact_select_vs_oracle(monkeypatch, integer_x):
 
 @pytest.mark.parametrize("bound", ["low", "overflow"])
 def test_fused_exact_select_fallbacks(monkeypatch, bound):
-    """A bound below the threshold (fewer than k kept) or one that keeps
-    more than the buffer holds falls back to the full statistics array."""
+    """A bound below the threshold (fewer than k kept) falls back to the full
+    statistics array; a kept buffer that overflows (here: sized for 1000
+    pairs) is refilled with the exact count, without the fallback."""
     from paper_2501_07642_b200 import _select as S
     monkeypatch.setattr(S, "PREFILTER_MIN", 1 << 20)
     h = 0 if bound == "low" else 0x7FF0000000000000  # +0.0 / +inf
     monkeypatch.setattr(S, "bound_from_sample", lambda *a: (h, 0.0))
-    calls = []
+    calls, caps = [], []
     real = G.exact_stats_device
     monkeypatch.setattr(G, "exact_stats_device", lambda *a, **kw: calls.append(1) or real(*a, **kw))
+    real_filter = G._narrow_filter
+
+    def record(kernel, design, lo, count, hb, cap):
+        caps.append(cap)
+        return real_filter(kernel, design, lo, count, hb, cap)
+
+    monkeypatch.setattr(G, "_narrow_filter", record)
+    monkeypatch.setattr(G, "KEPT_SLACK", 0.0)  # first buffer: 1000 pairs
+    monkeypatch.setattr(G, "KEPT_PAD", 1000)
     X = np.random.default_rng(3).standard_normal((26, 5))
     design = frr.DesignSpec(26, 13, accept_prob=1e-3, mode="exact")
     fused = frr.enumerate_exact(X, design)
-    assert calls == [1]  # the fallback ran pass 1 unfused
+    if bound == "low":
+        assert calls == [1]  # the fallback ran pass 1 unfused
+    else:
+        assert calls == [] and caps == [1000, math.comb(26, 13)], caps  # rerun with the exact count
     monkeypatch.undo()
     monkeypatch.setenv("FRR_EXACT_FUSED_SELECT", "0")
     plain = frr.enumerate_exact(X, design)
