@@ -264,9 +264,91 @@ def gen_rejection():
     np.savez_compressed(os.path.join(OUT, "rejection.npz"), **out)
 
 
+def _file_bytes(path) -> np.ndarray:
+    with open(path, "rb") as f:
+        return np.frombuffer(f.read(), dtype=np.uint8)
+
+
+def gen_poolio():
+    """Pool CSV files written by the reference (generation.py:388-525): Monte
+    Carlo pools in keys / full / both storage, streamed with out_path and
+    written with write_pool, and exact pools with and without out_path; plus
+    the reference's read_pool of each file."""
+    import dataclasses
+    import json
+    import tempfile
+
+    out = {}
+    X = np.random.default_rng(301).standard_normal((40, 3))
+    base = rg.DesignSpec(n_units=40, n_treated=20, accept_prob=0.01, max_draws=3000, batch_size=257,
+                         root_seed=301, precision_mode="exact")
+    Xe = np.random.default_rng(302).standard_normal((12, 3))
+    ex = rg.DesignSpec(n_units=12, n_treated=6, accept_prob=0.05, mode="exact", batch_size=100)
+    with tempfile.TemporaryDirectory() as d:
+        for storage in ("keys", "full", "both"):
+            design = dataclasses.replace(base, storage=storage)
+            path = os.path.join(d, f"mc_{storage}_stream.csv")
+            rg.generate_pool(X, design, workers=1, out_path=path)
+            out[f"mc_{storage}_stream"] = _file_bytes(path)
+            pool = rg.generate_pool(X, design, workers=1)
+            path = os.path.join(d, f"mc_{storage}_write.csv")
+            rg.write_pool(pool, path)
+            out[f"mc_{storage}_write"] = _file_bytes(path)
+        path = os.path.join(d, "exact_stream.csv")
+        rg.generate_pool(Xe, ex, out_path=path)
+        out["exact_stream"] = _file_bytes(path)
+        pool = rg.generate_pool(Xe, ex)
+        path = os.path.join(d, "exact_write.csv")
+        rg.write_pool(pool, path)
+        out["exact_write"] = _file_bytes(path)
+        # what the reference's reader makes of each file
+        for name in [k for k in out]:
+            path = os.path.join(d, name + ".csv")
+            with open(path, "wb") as f:
+                f.write(out[name].tobytes())
+            rp = rg.read_pool(path)
+            out[f"read_{name}"] = np.frombuffer(json.dumps({
+                "design": rp.design.to_json_dict(), "threshold": rp.threshold_value,
+                "n_candidates": rp.n_candidates, "stats": [repr(float(v)) for v in rp.stats],
+                "accepted": None if rp.accepted_indices is None else [int(v) for v in rp.accepted_indices],
+                "keys": None if rp.keys is None else [[int(a), int(b)] for a, b in rp.keys],
+                "assignments_sha": None if rp.assignments is None else sha(rp.assignments.astype(np.int8)),
+            }, sort_keys=True).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "poolio.npz"), **out)
+
+
+def gen_sweep():
+    """threshold_sweep rows of the reference (inference.py:279-312) with and
+    without the fiducial interval, including a failing row (accept_prob 0 is
+    an invalid design: row-level isolation)."""
+    import json
+
+    X = np.random.default_rng(311).standard_normal((30, 3))
+    rng = np.random.default_rng(312)
+    y = X @ rng.standard_normal(3) + 0.5 * rng.standard_normal(30)
+    base = rg.DesignSpec(n_units=30, n_treated=15, accept_prob=0.1, max_draws=4000, batch_size=500,
+                         root_seed=311, precision_mode="exact")
+    probs = [0.5, 0.1, 0.0, 0.02, 0.001]
+    out = {}
+    for find_fi in (False, True):
+        rows = ri.threshold_sweep(X, base, probs, y, find_fi=find_fi, alpha=0.1, workers=1)
+        out[f"rows_fi{int(find_fi)}"] = np.frombuffer(json.dumps(
+            [{k: (repr(v) if isinstance(v, float) else v) for k, v in r.items()} for r in rows]).encode(),
+            dtype=np.uint8)
+    exb = rg.DesignSpec(n_units=12, n_treated=6, accept_prob=0.1, mode="exact")
+    Xe = np.random.default_rng(313).standard_normal((12, 3))
+    ye = Xe[:, 0] + 0.3 * np.random.default_rng(314).standard_normal(12)
+    rows = ri.threshold_sweep(Xe, exb, [0.5, 0.2, 0.05, 0.01], ye, find_fi=True, alpha=0.2)
+    out["rows_exact"] = np.frombuffer(json.dumps(
+        [{k: (repr(v) if isinstance(v, float) else v) for k, v in r.items()} for r in rows]).encode(),
+        dtype=np.uint8)
+    out["probs"] = np.array(probs)
+    np.savez_compressed(os.path.join(OUT, "sweep.npz"), **out)
+
+
 GENERATORS = {"pairwise": lambda: gen_pairwise(), "keys": lambda: gen_keys(), "balance": lambda: gen_balance(),
               "pools": lambda: gen_pools(), "inference": lambda: gen_inference(), "sim": lambda: gen_sim(),
-              "rejection": lambda: gen_rejection()}
+              "rejection": lambda: gen_rejection(), "poolio": lambda: gen_poolio(), "sweep": lambda: gen_sweep()}
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
