@@ -7,10 +7,11 @@ alias below, so that every assertion the reference makes about its own
 public API is checked against paper_2501_07642_b200 (the B200 engine; there
 is no CPU path, so every test here needs the GPU and is marked ``gpu``).
 
-Exclusions (README.md in this directory): the timing-harness half of
-criterion 09 (run_benchmark's naive-vs-parallel CPU paths are the
-reference's benchmark harness, out of scope per SURVEY.md section 2.1),
-test_bench.py (same harness) and the matplotlib --plot CLI tests.
+Exclusions (README.md in this directory): criterion 09 (it times
+run_benchmark's naive-vs-parallel CPU paths, the reference's benchmark
+harness, out of scope per SURVEY.md section 2.1), test_bench.py (same
+harness) and the four CLI tests that render --plot figures (matplotlib is
+not installed; the reference fails them in this image too).
 """
 
 import importlib
@@ -54,9 +55,14 @@ def _alias():
 
 _alias()
 
+_PLOT = "--plot renders with matplotlib, which this image does not ship (the reference fails it here too)"
 EXCLUDED = {
     "test_acceptance.py::test_criterion_09_relative_speedup":
         "times the reference's naive/parallel CPU harness (run_benchmark), out of scope",
+    "test_cli.py::test_test_matches_library_and_emits_dist": _PLOT,
+    "test_cli.py::test_sweep_csv_and_plot": _PLOT,
+    "test_cli.py::test_bench_cli_schema": _PLOT + "; bench also names the reference's CPU harness paths",
+    "test_cli.py::test_generate_plot_written": _PLOT,
 }
 
 
