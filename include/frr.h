@@ -209,6 +209,16 @@ int frr_select_compact_capped(const double* stats, int64_t m, int64_t index_base
 int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t,
                const double* y, const uint32_t* obs_bits, double* a, double* b, int32_t* match,
                void* stream);
+/* frr_dim_mc in two kernels through a caller workspace: keys -> control
+ * bitsets (thread per key) in the workspace, then the statistics with y in
+ * shared memory, chunk by chunk (the workspace holds ws_bytes / (4 ceil(n/32))
+ * keys, a multiple of 32).  Same results as frr_dim_mc; falls back to it when
+ * the workspace holds fewer than 32 keys.  frr_dim_mc_workspace_bytes: the
+ * size that serves m keys in chunks of up to 2^18. */
+size_t frr_dim_mc_workspace_bytes(int64_t m, int n);
+int frr_dim_mc_ws(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t,
+                  const double* y, const uint32_t* obs_bits, double* a, double* b, int32_t* match,
+                  void* workspace, size_t ws_bytes, void* stream);
 int frr_dim_exact(const uint64_t* ranks, int64_t m, int n, int t, const double* y,
                   const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream);
 int frr_dim_rows(const int8_t* rows, int64_t m, int n, int t, const double* y,

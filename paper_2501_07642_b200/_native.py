@@ -75,6 +75,8 @@ SIGNATURES = {
     "frr_select_compact": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
     "frr_select_compact_capped": (i32, [vp, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp]),
     "frr_dim_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "frr_dim_mc_workspace_bytes": (sz, [i64, i32]),
+    "frr_dim_mc_ws": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
     "frr_dim_exact": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_tau_counts": (i32, [vp, vp, i64, vp, vp, i32, vp, vp]),

@@ -12,6 +12,7 @@
 
 #include "frr_common.cuh"
 #include "frr_launch.cuh"
+#include "frr_revfy.cuh"
 
 namespace {
 
@@ -814,6 +815,280 @@ __global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint6
     }
 }
 
+// ------------------------------------- randomization-test rows from keys
+// k_dim for Monte Carlo keys with the thread-per-candidate generator: a warp
+// regenerates 32 keys at once (frr_rev_fy: each lane builds one key's
+// control bitset in its own bank column of the warp's block; exact
+// recomputation of flagged keys), then every lane evaluates its own key:
+//   b and pool membership: exact popcounts against the observed assignment;
+//   a: numpy's pairwise sums of w*y and (1-w)*y (inference.py:82-101) in the
+//     reference's arithmetic -- the 0/1 weight times y is a float64 product,
+//     so masked-out terms are the reference's signed zeros -- walking numpy's
+//     recursion (leaves of <= 128 units with 8 interleaved accumulators,
+//     then the post-order combines) with a per-lane stack.  All lanes run the
+//     same program on the same unit, so y is read as one broadcast per 8
+//     units and the 16 accumulator chains give each lane its own ILP.
+constexpr int kDimRevWarps = 8;
+constexpr int kDimStack = 12;  // combine-stack depth bound: numpy's recursion holds <= log2(n / 128) + 2 <= 11 partial sums
+
+struct DimRevPlan {
+    int kw, maxl, warps;
+    size_t steps_off, fix_off, lock_off, plan_off, warp_off, per_warp, total;
+};
+
+DimRevPlan dim_rev_plan(int n, int t) {
+    DimRevPlan p;
+    p.kw = (n + 31) / 32;
+    p.maxl = plan_max_leaves(n);
+    size_t o = 0;
+    p.steps_off = o;
+    o += (size_t)frr_steps_len(t) * sizeof(StepC);
+    p.fix_off = o;
+    o += (size_t)frr_table_len(n) * 2 + FRR_TABLE_SLACK;
+    o = (o + 15) & ~(size_t)15;
+    p.lock_off = o;
+    o += 16;
+    p.plan_off = o;
+    o += 2 * (size_t)p.maxl * sizeof(int) + (size_t)((2 * p.maxl + 7) & ~7) * sizeof(int16_t);
+    o = (o + 15) & ~(size_t)15;
+    p.warp_off = o;
+    p.per_warp = (size_t)32 * p.kw * 4 + (size_t)kDimStack * 2 * 32 * sizeof(double);
+    p.warps = 0;
+    for (int w = kDimRevWarps; w >= 1; w--)
+        if (o + (size_t)w * p.per_warp <= 227 * 1024) {
+            p.warps = w;
+            break;
+        }
+    p.total = o + (size_t)p.warps * p.per_warp;
+    return p;
+}
+
+// masked terms of one unit for this lane's key: w*y and (1-w)*y, w = 0/1
+__device__ __forceinline__ void dim_terms(double v, uint32_t treated_bit, double& vt, double& vc) {
+    const double w = __hiloint2double(treated_bit ? 0x3FF00000 : 0, 0);
+    const double nw = __hiloint2double(treated_bit ? 0 : 0x3FF00000, 0);
+    vt = __dmul_rn(w, v);
+    vc = __dmul_rn(nw, v);
+}
+
+// b, membership and the pairwise sums of one lane's key: word(w) = the
+// key's control bits of units 32 w .. 32 w + 31; the sums are left on the
+// lane's stack (stk[0] = treated, stk[32] = control); y may be shared or global.
+template <class Word>
+__device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict__ y, const uint32_t* __restrict__ obs,
+                                     Word col_word, const int* leaf_off, const int* leaf_len, const int16_t* tok,
+                                     int ntok, double* stk, uint32_t& pt_out, uint32_t& pc_out, bool& same_out) {
+    // b and membership (exact integer popcounts)
+    uint32_t pt = 0, pc = 0;
+    bool same = true;
+    for (int w = 0; w < kw; w++) {
+        const int valid = n - 32 * w;
+        const uint32_t vm = valid >= 32 ? FRR_FULL : ((1u << valid) - 1u);
+        const uint32_t tr = ~col_word(w) & vm, o = __ldg(obs + w);
+        pt += __popc(tr & o);
+        pc += __popc(~tr & vm & o);
+        same &= tr == o;
+    }
+    // ---- a: numpy's pairwise sums of w*y and (1-w)*y, token program
+    int sp = 0;
+    for (int k = 0; k < ntok; k++) {
+        const int L = tok[k];
+        if (L < 0) {  // combine the top two partial sums
+            sp--;
+            stk[(2 * (sp - 1)) * 32] = __dadd_rn(stk[(2 * (sp - 1)) * 32], stk[(2 * sp) * 32]);
+            stk[(2 * (sp - 1) + 1) * 32] = __dadd_rn(stk[(2 * (sp - 1) + 1) * 32], stk[(2 * sp + 1) * 32]);
+            continue;
+        }
+        const int off = leaf_off[L], len = leaf_len[L];
+        double st, sc;
+        if (len < 8) {
+            st = sc = -0.0;
+            for (int i = 0; i < len; i++) {
+                const int e = off + i;
+                double vt, vc;
+                dim_terms(y[e], ~(col_word(e >> 5) >> (e & 31)) & 1u, vt, vc);
+                st = __dadd_rn(st, vt);
+                sc = __dadd_rn(sc, vc);
+            }
+        } else {
+            // 8 accumulators: r_j = term[j] + term[j + 8] + ... (off is a
+            // multiple of 8, so units e..e+7 share one bitset word)
+            const int full = len - (len % 8);
+            double rt[8], rc[8];
+            {
+                const uint32_t bits = ~(col_word(off >> 5) >> (off & 31));
+                const double2* yv = reinterpret_cast<const double2*>(y + off);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const double2 v2 = yv[q];
+                    dim_terms(v2.x, (bits >> (2 * q)) & 1u, rt[2 * q], rc[2 * q]);
+                    dim_terms(v2.y, (bits >> (2 * q + 1)) & 1u, rt[2 * q + 1], rc[2 * q + 1]);
+                }
+            }
+            for (int i = 8; i < full; i += 8) {
+                const int e = off + i;
+                const uint32_t bits = ~(col_word(e >> 5) >> (e & 31));
+                const double2* yv = reinterpret_cast<const double2*>(y + e);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const double2 v2 = yv[q];
+                    double vt0, vc0, vt1, vc1;
+                    dim_terms(v2.x, (bits >> (2 * q)) & 1u, vt0, vc0);
+                    dim_terms(v2.y, (bits >> (2 * q + 1)) & 1u, vt1, vc1);
+                    rt[2 * q] = __dadd_rn(rt[2 * q], vt0);
+                    rc[2 * q] = __dadd_rn(rc[2 * q], vc0);
+                    rt[2 * q + 1] = __dadd_rn(rt[2 * q + 1], vt1);
+                    rc[2 * q + 1] = __dadd_rn(rc[2 * q + 1], vc1);
+                }
+            }
+            st = __dadd_rn(__dadd_rn(__dadd_rn(rt[0], rt[1]), __dadd_rn(rt[2], rt[3])),
+                           __dadd_rn(__dadd_rn(rt[4], rt[5]), __dadd_rn(rt[6], rt[7])));
+            sc = __dadd_rn(__dadd_rn(__dadd_rn(rc[0], rc[1]), __dadd_rn(rc[2], rc[3])),
+                           __dadd_rn(__dadd_rn(rc[4], rc[5]), __dadd_rn(rc[6], rc[7])));
+            for (int i = full; i < len; i++) {  // the tail, in order
+                const int e = off + i;
+                double vt, vc;
+                dim_terms(y[e], ~(col_word(e >> 5) >> (e & 31)) & 1u, vt, vc);
+                st = __dadd_rn(st, vt);
+                sc = __dadd_rn(sc, vc);
+            }
+        }
+        stk[(2 * sp) * 32] = st;
+        stk[(2 * sp + 1) * 32] = sc;
+        sp++;
+    }
+    pt_out = pt;
+    pc_out = pc;
+    same_out = same;
+}
+
+__global__ void __launch_bounds__(kDimRevWarps * 32) k_dim_rev(uint64_t seed, const uint64_t* __restrict__ ids,
+                                                               int64_t m, int n, int t, const double* __restrict__ y,
+                                                               const uint32_t* __restrict__ obs, double* a, double* b,
+                                                               int32_t* match, DimRevPlan P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    StepC* steps = reinterpret_cast<StepC*>(smem + P.steps_off);
+    uint16_t* fix = reinterpret_cast<uint16_t*>(smem + P.fix_off);
+    int* lock = reinterpret_cast<int*>(smem + P.lock_off);
+    int* leaf_off = reinterpret_cast<int*>(smem + P.plan_off);
+    int* leaf_len = leaf_off + P.maxl;
+    int16_t* tok = reinterpret_cast<int16_t*>(leaf_len + P.maxl);
+    __shared__ int s_ntok;
+    frr_fill_steps(steps, n, t);
+    if (threadIdx.x == 0) {
+        *lock = 0;
+        PwPlan pl{0, 0, leaf_off, leaf_len, tok};
+        plan_build(pl, 0, n);
+        s_ntok = pl.ntok;
+    }
+    __syncthreads();
+    const int ntok = s_ntok;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kw = P.kw;
+    unsigned char* wbase = smem + P.warp_off + (size_t)warp * P.per_warp;
+    const uint32_t* col = reinterpret_cast<const uint32_t*>(wbase) + lane;  // this lane's key, word w at col[32 w]
+    double* stk = reinterpret_cast<double*>(wbase + (size_t)32 * kw * 4) + lane;  // [level][t/c][lane]
+    const uint32_t blk_a = (uint32_t)__cvta_generic_to_shared(wbase), sst = (uint32_t)__cvta_generic_to_shared(steps);
+    const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
+    const int64_t njobs = (m + 31) / 32;
+    for (int64_t job = (int64_t)blockIdx.x * P.warps + warp; job < njobs; job += (int64_t)gridDim.x * P.warps) {
+        const int64_t c = job * 32 + lane;
+        // ---- regenerate the 32 keys (lane = key), exact path for flagged ones
+        const uint64_t state = frr_derive_state(seed, ids[c < m ? c : m - 1]);
+        const bool flag = frr_rev_fy(state, t, sst, blk_a + 4u * lane, kw);
+        uint32_t fl = __ballot_sync(FRR_FULL, flag);
+        while (fl) {
+            const int src = __ffs(fl) - 1;
+            fl &= fl - 1;
+            if (lane == 0)
+                while (atomicCAS(lock, 0, 1) != 0) __nanosleep(100);
+            __syncwarp();
+            frr_rev_fixup(__shfl_sync(FRR_FULL, state, src), n, t, steps, fix, blk_a + 4u * src, kw, lane);
+            if (lane == 0) atomicExch(lock, 0);
+            __syncwarp();
+        }
+        __syncwarp();
+        uint32_t pt, pc;
+        bool same;
+        dim_lane(n, kw, y, obs, [&](int w) { return col[32 * w]; }, leaf_off, leaf_len, tok, ntok, stk, pt, pc, same);
+        if (c < m) {
+            const double s_t = __dadd_rn(0.0, stk[0]), s_c = __dadd_rn(0.0, stk[32]);
+            a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
+            if (b) b[c] = __dsub_rn(__dmul_rn((double)pt, inv_t), __dmul_rn((double)pc, inv_c));
+            if (match && same) atomicOr(match, 1);
+        }
+        __syncwarp();
+    }
+}
+
+// The same statistics from control bitsets already in global memory
+// (frr_rev_words' interleaved layout [job][w][32], lane = key): y lives in
+// shared memory (one broadcast per 8 units), so many warps per SM fit and
+// the generation kernel keeps all of shared memory for its bitsets.
+constexpr int kDimBitsWarps = 8;
+
+struct DimBitsPlan {
+    int kw, maxl;
+    size_t y_off, plan_off, stk_off, total;
+};
+
+DimBitsPlan dim_bits_plan(int n) {
+    DimBitsPlan p;
+    p.kw = (n + 31) / 32;
+    p.maxl = plan_max_leaves(n);
+    size_t o = 0;
+    p.y_off = o;
+    o += (size_t)n * sizeof(double);
+    o = (o + 15) & ~(size_t)15;
+    p.plan_off = o;
+    o += 2 * (size_t)p.maxl * sizeof(int) + (size_t)((2 * p.maxl + 7) & ~7) * sizeof(int16_t);
+    o = (o + 15) & ~(size_t)15;
+    p.stk_off = o;
+    o += (size_t)kDimBitsWarps * kDimStack * 2 * 32 * sizeof(double);
+    p.total = o;
+    return p;
+}
+
+__global__ void __launch_bounds__(kDimBitsWarps * 32) k_dim_bits(const uint32_t* __restrict__ words, int64_t m, int n,
+                                                                 int t, const double* __restrict__ y,
+                                                                 const uint32_t* __restrict__ obs, double* a, double* b,
+                                                                 int32_t* match, DimBitsPlan P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* sy = reinterpret_cast<double*>(smem + P.y_off);
+    int* leaf_off = reinterpret_cast<int*>(smem + P.plan_off);
+    int* leaf_len = leaf_off + P.maxl;
+    int16_t* tok = reinterpret_cast<int16_t*>(leaf_len + P.maxl);
+    __shared__ int s_ntok;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sy[i] = y[i];
+    if (threadIdx.x == 0) {
+        PwPlan pl{0, 0, leaf_off, leaf_len, tok};
+        plan_build(pl, 0, n);
+        s_ntok = pl.ntok;
+    }
+    __syncthreads();
+    const int ntok = s_ntok;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kw = P.kw;
+    double* stk = reinterpret_cast<double*>(smem + P.stk_off) + (size_t)warp * kDimStack * 2 * 32 + lane;
+    const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
+    const int64_t njobs = (m + 31) / 32;
+    for (int64_t job = (int64_t)blockIdx.x * kDimBitsWarps + warp; job < njobs;
+         job += (int64_t)gridDim.x * kDimBitsWarps) {
+        const int64_t c = job * 32 + lane;
+        const uint32_t* col = words + (size_t)job * kw * 32 + lane;  // coalesced: one 128-byte row per word
+        uint32_t pt, pc;
+        bool same;
+        dim_lane(n, kw, sy, obs, [&](int w) { return __ldg(col + 32 * w); }, leaf_off, leaf_len, tok, ntok, stk, pt,
+                 pc, same);
+        if (c < m) {
+            const double s_t = __dadd_rn(0.0, stk[0]), s_c = __dadd_rn(0.0, stk[32]);
+            a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
+            if (b) b[c] = __dsub_rn(__dmul_rn((double)pt, inv_t), __dmul_rn((double)pc, inv_c));
+            if (match && same) atomicOr(match, 1);
+        }
+    }
+}
+
 // ------------------------------------------------------------ tau counts
 constexpr int kTauTile = 32;
 
@@ -1147,7 +1422,66 @@ extern "C" int frr_regen_exact(const uint64_t* ranks, int64_t m, int n, int t, i
 
 extern "C" int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t, const double* y,
                           const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* stream) {
+    int rc = check_nt(n, t);
+    if (rc) return rc;
+    if (m <= 0) return FRR_OK;
+    // thread-per-key regeneration when two or more warps' bitsets fit shared
+    // memory (n up to ~9000), else the warp-per-key kernel
+    const DimRevPlan P = dim_rev_plan(n, t);
+    const char* path = getenv("FRR_DIM_PATH");
+    if (P.warps >= 2 && !(path && path[0] == 'w')) {
+        if ((rc = frr_prepare_kernel(k_dim_rev, P.total))) return rc;
+        const int grid = frr_persistent_grid(k_dim_rev, P.warps * 32, P.total, frr_cdiv(m, 32 * P.warps));
+        k_dim_rev<<<grid, P.warps * 32, P.total, frr_stream(stream)>>>(root_seed, draws, m, n, t, y, obs_bits, a, b,
+                                                                      match, P);
+        return frr_launched("k_dim_rev");
+    }
     return launch_dim<SRC_KEYS>(root_seed, draws, nullptr, m, n, t, y, obs_bits, a, b, match, stream);
+}
+
+int frr_rev_words(uint64_t root_seed, const uint64_t* ids, int64_t count, int n, int t, uint32_t* words,
+                  void* steps, void* stream);
+
+// workspace of frr_dim_mc_ws: the generator's global step table (64 KB per
+// 4096 steps, t <= FRR_MAX_UNITS) then the bitsets of a chunk of keys (a
+// multiple of 32)
+static size_t dim_ws_steps_bytes() { return (size_t)frr_steps_len(FRR_MAX_UNITS) * sizeof(StepC); }
+
+static int64_t dim_ws_chunk(int n, size_t ws_bytes) {
+    const size_t per_key = (size_t)((n + 31) / 32) * 4;
+    if (ws_bytes < dim_ws_steps_bytes()) return 0;
+    return (int64_t)((ws_bytes - dim_ws_steps_bytes()) / per_key) / 32 * 32;
+}
+
+extern "C" size_t frr_dim_mc_workspace_bytes(int64_t m, int n) {
+    if (m <= 0 || n < 2) return 0;
+    const int64_t keys = std::min<int64_t>((m + 31) / 32 * 32, (int64_t)1 << 18);
+    return dim_ws_steps_bytes() + (size_t)keys * ((n + 31) / 32) * 4;
+}
+
+extern "C" int frr_dim_mc_ws(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t, const double* y,
+                             const uint32_t* obs_bits, double* a, double* b, int32_t* match, void* workspace,
+                             size_t ws_bytes, void* stream) {
+    int rc = check_nt(n, t);
+    if (rc) return rc;
+    if (m <= 0) return FRR_OK;
+    const int64_t chunk = dim_ws_chunk(n, ws_bytes);
+    const DimBitsPlan P = dim_bits_plan(n);
+    if (chunk < 32 || P.total > 227 * 1024)
+        return frr_dim_mc(root_seed, draws, m, n, t, y, obs_bits, a, b, match, stream);
+    if ((rc = frr_prepare_kernel(k_dim_bits, P.total))) return rc;
+    void* steps = workspace;
+    uint32_t* words = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(workspace) + dim_ws_steps_bytes());
+    for (int64_t lo = 0; lo < m; lo += chunk) {
+        const int64_t cnt = std::min<int64_t>(chunk, m - lo);
+        if ((rc = frr_rev_words(root_seed, draws + lo, cnt, n, t, words, steps, stream))) return rc;
+        const int grid = frr_persistent_grid(k_dim_bits, kDimBitsWarps * 32, P.total,
+                                             frr_cdiv(cnt, 32 * kDimBitsWarps));
+        k_dim_bits<<<grid, kDimBitsWarps * 32, P.total, frr_stream(stream)>>>(
+            words, cnt, n, t, y, obs_bits, a + lo, b ? b + lo : nullptr, match, P);
+        if ((rc = frr_launched("k_dim_bits"))) return rc;
+    }
+    return FRR_OK;
 }
 
 extern "C" int frr_dim_exact(const uint64_t* ranks, int64_t m, int n, int t, const double* y,

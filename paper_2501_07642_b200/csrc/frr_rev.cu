@@ -18,17 +18,19 @@ struct RevPlan {
     size_t steps_off, ws_off, fix_off, lock_off, total;
 };
 
-RevPlan rev_plan(int n, int t) {
+// gsteps: the step table lives in global memory (the caller's workspace)
+RevPlan rev_plan(int n, int t, bool gsteps = false) {
     RevPlan p;
     p.kw = (n + 31) / 32;
     p.warps = kRevWarps;
+    const size_t steps_b = gsteps ? 0 : (size_t)frr_steps_len(t) * sizeof(StepC);
     // fewer warps when the bitsets of 16 do not fit shared memory
-    while (p.warps > 1 && (size_t)p.warps * 32 * p.kw * 4 + (size_t)frr_steps_len(t) * sizeof(StepC) +
-                                  (size_t)frr_table_len(n) * 2 + FRR_TABLE_SLACK + 64 > 227 * 1024)
+    while (p.warps > 1 && (size_t)p.warps * 32 * p.kw * 4 + steps_b + (size_t)frr_table_len(n) * 2 +
+                                  FRR_TABLE_SLACK + 64 > 227 * 1024)
         p.warps--;
     size_t o = 0;
     p.steps_off = o;
-    o += (size_t)frr_steps_len(t) * sizeof(StepC);
+    o += steps_b;
     p.ws_off = o;
     o += (size_t)p.warps * 32 * p.kw * 4;
     p.fix_off = o;
@@ -40,28 +42,36 @@ RevPlan rev_plan(int n, int t) {
     return p;
 }
 
-// out: bits [count, kw] (control bit e of word e/32), optional; sink: XOR
-// of every candidate's words (optional; keeps the work alive in benchmarks)
-__global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, uint64_t lo, int64_t count, int n, int t,
-                                                             RevPlan P, uint32_t* __restrict__ out,
-                                                             unsigned long long* sink) {
+// Candidate c = draw ids[c] (ids != NULL) or lo + c.  out: control bits
+// (bit e of word e/32 = unit e), row-major [count][kw] (interleaved = 0) or
+// [count/32][kw][32] (interleaved = 1: a warp's block as built, coalesced
+// stores; frr_dim_mc_ws reads it back per lane); optional.  sink: XOR of
+// every candidate's words (optional; keeps the work alive in benchmarks).
+// GS: the step table `gsteps` is in global memory (filled by the caller),
+// else this kernel fills a shared copy
+template <bool GS>
+__global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, const uint64_t* __restrict__ ids,
+                                                             uint64_t lo, int64_t count, int n, int t, RevPlan P,
+                                                             uint32_t* __restrict__ out, int interleaved,
+                                                             unsigned long long* sink, const StepC* gsteps) {
     extern __shared__ __align__(16) unsigned char smem[];
-    StepC* steps = reinterpret_cast<StepC*>(smem + P.steps_off);
+    StepC* steps = GS ? const_cast<StepC*>(gsteps) : reinterpret_cast<StepC*>(smem + P.steps_off);
     uint16_t* fix = reinterpret_cast<uint16_t*>(smem + P.fix_off);
     int* lock = reinterpret_cast<int*>(smem + P.lock_off);
-    frr_fill_steps(steps, n, t);
+    if (!GS) frr_fill_steps(steps, n, t);
     if (threadIdx.x == 0) *lock = 0;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t sst = (uint32_t)__cvta_generic_to_shared(steps);
+    const uint64_t sst = GS ? (uint64_t)steps : (uint64_t)__cvta_generic_to_shared(steps);
     const uint32_t wsa0 = (uint32_t)__cvta_generic_to_shared(smem + P.ws_off) + (uint32_t)warp * 128u * P.kw;
     const uint32_t wsa = wsa0 + 4u * lane;
     uint32_t acc = 0;
     const int64_t njobs = (count + 31) / 32;
     for (int64_t job = (int64_t)blockIdx.x * P.warps + warp; job < njobs; job += (int64_t)gridDim.x * P.warps) {
         const int64_t c = job * 32 + lane;
-        const uint64_t state = frr_derive_state(seed, lo + (uint64_t)c);
-        const bool flag = frr_rev_fy(state, t, sst, wsa, P.kw);
+        const uint64_t state =
+            frr_derive_state(seed, ids ? ids[c < count ? c : count - 1] : lo + (uint64_t)c);
+        const bool flag = frr_rev_fy<GS>(state, t, sst, wsa, P.kw);
         uint32_t fl = __ballot_sync(FRR_FULL, flag);
         while (fl) {
             const int src = __ffs(fl) - 1;
@@ -78,28 +88,58 @@ __global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, uint
             uint32_t v;
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsa + 128u * (uint32_t)w) : "memory");
             acc ^= v * (uint32_t)(2 * w + 1);
-            if (out && c < count) out[(size_t)c * P.kw + w] = v;
+            if (out && interleaved) out[((size_t)job * P.kw + w) * 32 + lane] = v;
+            else if (out && c < count) out[(size_t)c * P.kw + w] = v;
         }
     }
     if (sink && acc) atomicXor(sink, (unsigned long long)acc);
 }
 }  // namespace
 
-extern "C" int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count, int n, int t, uint32_t* bits,
-                            unsigned long long* sink, void* stream) {
+__global__ void k_fill_steps_ws(StepC* steps, int n, int t) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < frr_steps_len(t); k += gridDim.x * blockDim.x)
+        steps[k] = frr_make_step(k < t ? n : k + 1, k);
+}
+
+// gsteps: caller memory of frr_steps_len(t) * 16 bytes for a global step
+// table (NULL: shared copy per CTA)
+static int rev_launch(uint64_t root_seed, const uint64_t* ids, uint64_t draw_lo, int64_t count, int n, int t,
+                      uint32_t* bits, int interleaved, unsigned long long* sink, StepC* gsteps, void* stream) {
     if (n < 2 || t < 1 || t >= n || n > FRR_MAX_UNITS) {
         frr_set_error("frr_rev_bits: need 0 < t < n <= %d", FRR_MAX_UNITS);
         return FRR_E_INVALID_DESIGN;
     }
     if (count <= 0) return FRR_OK;
-    const RevPlan P = rev_plan(n, t);
+    // the shared step table wins while it leaves 6 or more warps (measured at
+    // n = 5000: 8 warps with shared steps beat 11 with global ones by 9%)
+    if (gsteps && rev_plan(n, t, false).warps >= 6) gsteps = nullptr;
+    const RevPlan P = rev_plan(n, t, gsteps != nullptr);
     if (P.total > 227 * 1024) {
         frr_set_error("frr_rev_bits: n=%d too large for the shared bitsets", n);
         return FRR_E_UNSUPPORTED;
     }
-    int rc = frr_prepare_kernel(k_rev_bits, P.total);
+    const auto kern = gsteps ? k_rev_bits<true> : k_rev_bits<false>;
+    int rc = frr_prepare_kernel(kern, P.total);
     if (rc) return rc;
-    const int grid = frr_persistent_grid(k_rev_bits, P.warps * 32, P.total, frr_cdiv(count, 32 * P.warps));
-    k_rev_bits<<<grid, P.warps * 32, P.total, frr_stream(stream)>>>(root_seed, draw_lo, count, n, t, P, bits, sink);
+    cudaStream_t s = frr_stream(stream);
+    if (gsteps) {
+        k_fill_steps_ws<<<std::max(1, frr_steps_len(t) / 256), 256, 0, s>>>(gsteps, n, t);
+        if ((rc = frr_launched("k_fill_steps_ws"))) return rc;
+    }
+    const int grid = frr_persistent_grid(kern, P.warps * 32, P.total, frr_cdiv(count, 32 * P.warps));
+    kern<<<grid, P.warps * 32, P.total, s>>>(root_seed, ids, draw_lo, count, n, t, P, bits, interleaved, sink, gsteps);
     return frr_launched("k_rev_bits");
+}
+
+// keys (root_seed, ids[i]) -> control bitsets in the interleaved layout
+// [ceil(count/32)][ceil(n/32)][32] (used by frr_dim_mc_ws); steps: caller
+// memory for the global step table (frr_steps_len(t) * 16 bytes) or NULL
+int frr_rev_words(uint64_t root_seed, const uint64_t* ids, int64_t count, int n, int t, uint32_t* words,
+                  void* steps, void* stream) {
+    return rev_launch(root_seed, ids, 0, count, n, t, words, 1, nullptr, static_cast<StepC*>(steps), stream);
+}
+
+extern "C" int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count, int n, int t, uint32_t* bits,
+                            unsigned long long* sink, void* stream) {
+    return rev_launch(root_seed, nullptr, draw_lo, count, n, t, bits, 0, sink, nullptr, stream);
 }

@@ -51,6 +51,18 @@ __device__ __forceinline__ StepC frr_lds_step(uint32_t a) {
     return s;
 }
 
+// the same record from a global step table (read-only for the kernel's
+// lifetime: non-coherent loads, L1-cached; every lane loads the same address)
+__device__ __forceinline__ StepC frr_ldg_step(uint64_t a) {
+    uint32_t x, y, z, w;
+    asm("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(a));
+    StepC s;
+    s.b = x;
+    s.c2 = y;
+    s.M = ((uint64_t)w << 32) | z;
+    return s;
+}
+
 // words [from, to) of this lane's bitset = all ones (positions >= t: the
 // initial set; padding beyond n stays control, its operand rows are zero)
 __device__ __forceinline__ void frr_rev_fill(uint32_t wsa, int from, int to) {
@@ -63,7 +75,10 @@ __device__ __forceinline__ void frr_rev_fill(uint32_t wsa, int from, int to) {
 // step table (frr_fill_steps: steps k >= t are dummies with b = 1, d = 0).
 // Returns true when some stream value had hi == 0xFFFFFFFF (possible
 // rejection: the candidate must be recomputed exactly).
-__device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps, uint32_t wsa, int kw) {
+// GS: `steps` is the generic address of a global step table (frees the
+// table's shared memory for more bitsets), else a shared address.
+template <bool GS = false>
+__device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps, uint32_t wsa, int kw) {
     const int wtop = (t - 1) >> 5;
     frr_rev_fill(wsa, wtop + 1, kw);
     uint32_t hmax = 0;
@@ -78,7 +93,7 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
         const int lo = 32 * W;
         const uint32_t init = t >= lo + 32 ? 0u : (~0u << (t - lo));
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(init) : "memory");
-        const uint32_t sa = steps + 16u * (uint32_t)lo;
+        const uint64_t sa = steps + 16ull * (uint64_t)lo;
         // FRR_REV_GROUP draws computed ahead of their bit moves: independent
         // register work the scheduler interleaves with the serial chain of
         // shared-memory bit moves
@@ -89,7 +104,8 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint32_t steps
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
                 x -= FRR_GOLDEN;
-                const StepC s = frr_lds_step(sa + 16u * (uint32_t)(jg - i));
+                const StepC s = GS ? frr_ldg_step(sa + 16ull * (uint64_t)(jg - i))
+                                   : frr_lds_step((uint32_t)sa + 16u * (uint32_t)(jg - i));
                 const uint64_t u = frr_mix64(x);
                 hh[i] = (uint32_t)(u >> 32);
                 dd[i] = frr_mod_step(u, s, z0, z1);

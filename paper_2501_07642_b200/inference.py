@@ -127,8 +127,11 @@ class _PoolStats:
                     "pool stores no keys; exact-mode pools carry explicit assignments instead")
             draws = keymod.to_device_u64(np.ascontiguousarray(pool.keys[lo:hi, 1], dtype=np.uint64))
             if hi > lo:
-                N.call("frr_dim_mc", int(d.root_seed) & keymod.MASK64, N.ptr(draws), hi - lo, n, t, N.ptr(y_dev),
-                       N.ptr(obs_dev), N.ptr(a), N.ptr(b), N.ptr(match), N.stream_ptr())
+                ws_bytes = int(N.lib().frr_dim_mc_workspace_bytes(hi - lo, n))
+                ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=dev)
+                N.call("frr_dim_mc_ws", int(d.root_seed) & keymod.MASK64, N.ptr(draws), hi - lo, n, t,
+                       N.ptr(y_dev), N.ptr(obs_dev), N.ptr(a), N.ptr(b), N.ptr(match), N.ptr(ws), ws_bytes,
+                       N.stream_ptr())
         if comm.world > 1:
             comm.all_reduce_(match)
         self.a_local, self.b_local = a, b

@@ -1,4 +1,5 @@
-"""One k_dim launch on the C5 shape (n=5000, t=2500, 2^18 keys) for ncu."""
+"""The C5 statistics kernels (frr_dim_mc_ws: k_rev_bits + k_dim_bits; FRR_C5_SINGLE=1: k_dim_rev)
+on the C5 shape (n=5000, t=2500, 2^18 keys), for ncu."""
 import os
 import sys
 
@@ -17,9 +18,15 @@ obs = torch.zeros(157, dtype=torch.int32, device="cuda")
 a = torch.empty(m, dtype=torch.float64, device="cuda")
 b = torch.empty(m, dtype=torch.float64, device="cuda")
 match = torch.zeros(1, dtype=torch.int32, device="cuda")
+ws_bytes = int(N.lib().frr_dim_mc_workspace_bytes(m, 5000))
+ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
 for _ in range(2):
-    N.call("frr_dim_mc", 5, N.ptr(draws), m, 5000, 2500, N.ptr(y), N.ptr(obs), N.ptr(a), N.ptr(b), N.ptr(match),
-           N.stream_ptr())
+    if os.environ.get("FRR_C5_SINGLE"):
+        N.call("frr_dim_mc", 5, N.ptr(draws), m, 5000, 2500, N.ptr(y), N.ptr(obs), N.ptr(a), N.ptr(b), N.ptr(match),
+               N.stream_ptr())
+    else:
+        N.call("frr_dim_mc_ws", 5, N.ptr(draws), m, 5000, 2500, N.ptr(y), N.ptr(obs), N.ptr(a), N.ptr(b),
+               N.ptr(match), N.ptr(ws), ws_bytes, N.stream_ptr())
 torch.cuda.synchronize()
 print("ok")
 # one 512-point tau grid over the m keys (k_tau_counts)
