@@ -30,11 +30,11 @@
 #ifndef FRR_REV_GROUP
 #define FRR_REV_GROUP 8  // draws computed ahead of their bit moves (divides 32)
 #endif
+#ifndef FRR_REV_PIPE
+#define FRR_REV_PIPE 0  // 1: draws of the next group issued ahead of the current group's bit moves (measured: no gain, 2x registers)
+#endif
 #ifndef FRR_REV_FETCH_AND
 #define FRR_REV_FETCH_AND 1  // 1: atom.and fetch-and-clear for the r-side bit
-#endif
-#ifndef FRR_REV_JSIDE
-#define FRR_REV_JSIDE 0  // 0: shared atomic OR for the j-side bit, 1: load/or/store
 #endif
 
 // one step-constant record (b, c2, M) of the shared step table; pure
@@ -77,99 +77,110 @@ __device__ __forceinline__ void frr_rev_fill(uint32_t wsa, int from, int to) {
 // rejection: the candidate must be recomputed exactly).
 // GS: `steps` is the generic address of a global step table (frees the
 // table's shared memory for more bitsets), else a shared address.
+// One reverse step's bit move: fetch-and-clear bit r (= 32 W + e) of the
+// r-side word, OR it into bit jb = e - d of word W (address wa).  Program
+// order of one thread's shared accesses keeps the r == j and same-word
+// cases right.
+__device__ __forceinline__ void frr_rev_move(uint32_t wa, uint32_t e, uint32_t d) {
+    uint32_t ra;  // r's word is W + e / 32
+    asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
+#if FRR_REV_FETCH_AND
+    // nm = ~(1 << (e & 31)); the rotation of the isolated bit right by d lands it on jb
+    asm volatile(
+        "{\n\t.reg .u32 w, c, nm, v;\n\t"
+        "shf.l.wrap.b32 nm, %4, %4, %1;\n\t"
+        "atom.shared.and.b32 w, [%0], nm;\n\t"
+        "lop3.b32 c, w, nm, 0, 0x30;\n\t"  // w & ~nm
+        "shf.r.wrap.b32 v, c, c, %3;\n\t"
+        "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
+        "r"(e), "r"(wa), "r"(d), "r"(0xFFFFFFFEu)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .u32 w, c, m, v;\n\t"
+        "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
+        "ld.shared.u32 w, [%0];\n\t"
+        "and.b32 c, w, m;\n\t"
+        "xor.b32 w, w, c;\n\t"
+        "st.shared.u32 [%0], w;\n\t"
+        "shf.r.wrap.b32 v, c, c, %3;\n\t"
+        "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
+        "r"(e), "r"(wa), "r"(d)
+        : "memory");
+#endif
+}
+
+// FRR_REV_GROUP draws of consecutive steps (descending j from the record at
+// address sa): d values and the running max of hi(u).  x = state + (j+1) C
+// of the next step, decremented per draw.
+template <bool GS>
+__device__ __forceinline__ void frr_rev_draws(uint64_t& x, uint64_t sa, uint32_t z0, uint32_t z1,
+                                              uint32_t (&dd)[FRR_REV_GROUP], uint32_t& hmax) {
+    uint32_t hh[FRR_REV_GROUP];
+#pragma unroll
+    for (int i = 0; i < FRR_REV_GROUP; i++) {
+        x -= FRR_GOLDEN;
+        const StepC s = GS ? frr_ldg_step(sa - 16ull * (uint64_t)i) : frr_lds_step((uint32_t)sa - 16u * (uint32_t)i);
+        const uint64_t u = frr_mix64(x);
+        hh[i] = (uint32_t)(u >> 32);
+        dd[i] = frr_mod_step(u, s, z0, z1);
+    }
+    // a rejection needs hi(u) == 0xFFFFFFFF: running max, two draws per three-input max
+#pragma unroll
+    for (int i = 0; i + 1 < FRR_REV_GROUP; i += 2) hmax = max(hmax, max(hh[i], hh[i + 1]));
+    if (FRR_REV_GROUP & 1) hmax = max(hmax, hh[FRR_REV_GROUP - 1]);
+}
+
+// Builds the control bitset of candidate `state` into this lane's column of
+// the warp's bitset block (wsa = shared address of word 0 of this lane).
+// kw words are written (kw >= ceil(n / 32)).  steps: shared address of the
+// step table (frr_fill_steps: steps k >= t are dummies with b = 1, d = 0);
+// GS: the generic address of a global step table instead.
+// Returns true when some stream value had hi == 0xFFFFFFFF (possible
+// rejection: the candidate must be recomputed exactly).
+//
+// Software-pipelined: the draws of the next FRR_REV_GROUP steps are issued
+// ahead of the current group's bit moves, so their independent register
+// work fills the latency of the serial shared-memory chain (each move's
+// atomic must return before its OR).
 template <bool GS = false>
 __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps, uint32_t wsa, int kw) {
+    constexpr int GPW = 32 / FRR_REV_GROUP;  // groups per 32-step word block
     const int wtop = (t - 1) >> 5;
     frr_rev_fill(wsa, wtop + 1, kw);
     uint32_t hmax = 0;
     // zeros opaque to the compiler: the high words of frr_mod_step's 64-bit
     // addends stay live instead of being re-zeroed every draw
     uint32_t z0 = (uint32_t)t >> 31, z1 = (uint32_t)(t + 1) >> 31;
-    // x = state + (j + 1) C for the step j about to run
+    // x = state + (j + 1) C for the step j about to be drawn
     uint64_t x = state + (uint64_t)(32 * wtop + 33) * FRR_GOLDEN;
+    uint64_t sa = steps + 16ull * (uint64_t)(32 * wtop + 31);  // record of the next step to draw
+    uint32_t dn[FRR_REV_GROUP];
+    frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
+    sa -= 16ull * FRR_REV_GROUP;
     for (int W = wtop; W >= 0; W--) {
         const uint32_t wa = wsa + 128u * (uint32_t)W;
         // word W before its own steps: positions >= t set
         const int lo = 32 * W;
         const uint32_t init = t >= lo + 32 ? 0u : (~0u << (t - lo));
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(init) : "memory");
-        const uint64_t sa = steps + 16ull * (uint64_t)lo;
-        // FRR_REV_GROUP draws computed ahead of their bit moves: independent
-        // register work the scheduler interleaves with the serial chain of
-        // shared-memory bit moves
 #pragma unroll
-        for (int jg = 31; jg >= 0; jg -= FRR_REV_GROUP) {
+        for (int q = 0; q < GPW; q++) {
             uint32_t dd[FRR_REV_GROUP];
-            uint32_t hh[FRR_REV_GROUP];
 #pragma unroll
-            for (int i = 0; i < FRR_REV_GROUP; i++) {
-                x -= FRR_GOLDEN;
-                const StepC s = GS ? frr_ldg_step(sa + 16ull * (uint64_t)(jg - i))
-                                   : frr_lds_step((uint32_t)sa + 16u * (uint32_t)(jg - i));
-                const uint64_t u = frr_mix64(x);
-                hh[i] = (uint32_t)(u >> 32);
-                dd[i] = frr_mod_step(u, s, z0, z1);
+            for (int i = 0; i < FRR_REV_GROUP; i++) dd[i] = dn[i];
+            if (FRR_REV_PIPE && (q < GPW - 1 || W > 0)) {  // the next group (the last one has none)
+                frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
+                sa -= 16ull * FRR_REV_GROUP;
             }
-            // a rejection needs hi(u) == 0xFFFFFFFF: running max, two draws per
-            // three-input max
-#pragma unroll
-            for (int i = 0; i + 1 < FRR_REV_GROUP; i += 2) hmax = max(hmax, max(hh[i], hh[i + 1]));
-            if (FRR_REV_GROUP & 1) hmax = max(hmax, hh[FRR_REV_GROUP - 1]);
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
-                const int jb = jg - i;
-                const uint32_t d = dd[i];
-                // e = r - 32 W: r's word is W + e / 32
-                const uint32_t e = (uint32_t)jb + d;
-                uint32_t ra;
-                asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}"
-                    : "=r"(ra)
-                    : "r"(e), "r"(wa));
-#if FRR_REV_JSIDE == 0
-                // r-side: read the word, clear bit r; j-side: OR the bit into
-                // word W (its bit jb is 0 until now) -- rotating the isolated
-                // bit r & 31 right by d lands it on jb.  Program order of one
-                // thread's shared accesses keeps the r == j and same-word
-                // cases right.
-#if FRR_REV_FETCH_AND
-                // fetch-and-clear of bit r in one shared atomic (nm = ~m)
-                asm volatile(
-                    "{\n\t.reg .u32 w, c, nm, v;\n\t"
-                    "shf.l.wrap.b32 nm, %4, %4, %1;\n\t"
-                    "atom.shared.and.b32 w, [%0], nm;\n\t"
-                    "lop3.b32 c, w, nm, 0, 0x30;\n\t"  // w & ~nm
-                    "shf.r.wrap.b32 v, c, c, %3;\n\t"
-                    "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
-                    "r"(e), "r"(wa), "r"(d), "r"(0xFFFFFFFEu)
-                    : "memory");
-#else
-                asm volatile(
-                    "{\n\t.reg .u32 w, c, m, v;\n\t"
-                    "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
-                    "ld.shared.u32 w, [%0];\n\t"
-                    "and.b32 c, w, m;\n\t"
-                    "xor.b32 w, w, c;\n\t"
-                    "st.shared.u32 [%0], w;\n\t"
-                    "shf.r.wrap.b32 v, c, c, %3;\n\t"
-                    "red.shared.or.b32 [%2], v;\n\t}" ::"r"(ra),
-                    "r"(e), "r"(wa), "r"(d)
-                    : "memory");
-#endif
-#else
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\t.reg .u32 w, c, m, v;\n\t"
-                    "shf.l.wrap.b32 m, 1, 1, %1;\n\t"
-                    "ld.shared.u32 w, [%0];\n\t"
-                    "and.b32 c, w, m;\n\t"
-                    "setp.ne.u32 p, c, 0;\n\t"
-                    "xor.b32 w, w, c;\n\t"
-                    "st.shared.u32 [%0], w;\n\t"
-                    "ld.shared.u32 v, [%2];\n\t"
-                    "@p or.b32 v, v, %3;\n\t"
-                    "st.shared.u32 [%2], v;\n\t}" ::"r"(ra),
-                    "r"(e), "r"(wa), "n"(1u << jb)
-                    : "memory");
-#endif
+                const int jb = 31 - q * FRR_REV_GROUP - i;
+                frr_rev_move(wa, (uint32_t)jb + dd[i], dd[i]);
+            }
+            if (!FRR_REV_PIPE && (q < GPW - 1 || W > 0)) {
+                frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
+                sa -= 16ull * FRR_REV_GROUP;
             }
         }
     }
