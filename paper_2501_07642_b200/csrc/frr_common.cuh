@@ -10,6 +10,20 @@
 #include "../../include/frr.h"
 
 #define FRR_GOLDEN 0x9E3779B97F4A7C15ull
+
+// Device-side bounds / invariant checks of the FRR_CHECKS=1 diagnostic build
+// (make checks): a failed check traps the kernel with its location.  The
+// pool's GPUs run no compute-sanitizer, so these asserts plus oracle
+// comparisons on small cases are the memory-safety evidence.
+#ifndef FRR_CHECKS
+#define FRR_CHECKS 0
+#endif
+#if FRR_CHECKS
+#include <assert.h>
+#define FRR_CHECK(c) assert(c)
+#else
+#define FRR_CHECK(c) ((void)0)
+#endif
 #define FRR_FULL 0xffffffffu
 #define FRR_CTL 0xFFFFu  // table marker: unit is a control unit
 
@@ -128,7 +142,9 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
     s.M = ((uint64_t)q.w << 32) | q.z;
     const uint64_t u = frr_mix64(x);
     hmax = max(hmax, (uint32_t)(u >> 32));  // a rejection needs hi(u) == 0xFFFFFFFF
-    return frr_mod_step(u, s, zero, zero2);
+    const uint32_t d = frr_mod_step(u, s, zero, zero2);
+    FRR_CHECK(d < s.b && d == (uint32_t)(u % s.b));
+    return d;
 }
 
 #ifndef FRR_FY_ROUNDS
@@ -298,6 +314,7 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
                     u = frr_mix64(s);
                 } while (rem != 0 && u >= 0ull - rem);
                 uint32_t r = (uint32_t)j + (uint32_t)(u % b);
+                FRR_CHECK(r < (uint32_t)n);
                 if (r != (uint32_t)j) lw[r] = (uint16_t)(j + 1);
             }
         }

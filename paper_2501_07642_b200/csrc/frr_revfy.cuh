@@ -124,6 +124,7 @@ __device__ __forceinline__ void frr_rev_draws(uint64_t& x, uint64_t sa, uint32_t
         const uint64_t u = frr_mix64(x);
         hh[i] = (uint32_t)(u >> 32);
         dd[i] = frr_mod_step(u, s, z0, z1);
+        FRR_CHECK(dd[i] < s.b && dd[i] == (uint32_t)(u % s.b));
     }
     // a rejection needs hi(u) == 0xFFFFFFFF: running max, two draws per three-input max
 #pragma unroll
@@ -176,6 +177,7 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
                 const int jb = 31 - q * FRR_REV_GROUP - i;
+                FRR_CHECK(32 * W + jb + (int)dd[i] < 32 * kw);  // r inside this lane's bitset
                 frr_rev_move(wa, (uint32_t)jb + dd[i], dd[i]);
             }
             if (!FRR_REV_PIPE && (q < GPW - 1 || W > 0)) {
