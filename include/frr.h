@@ -200,6 +200,15 @@ int frr_select_compact_capped(const double* stats, int64_t m, int64_t index_base
                               const int64_t* tie_quota, int64_t cap, int64_t* idx_out, double* stat_out,
                               int64_t* n_out, void* workspace, void* stream);
 
+/* Stable LSD radix sort of n (key, value) pairs by the low key_bits of the
+ * uint64 keys, in place (values: any 8-byte payload).  The fused exact pass
+ * keeps (rank, statistic) pairs in arrival order; this puts them in rank
+ * order for the select (generation.py:159-169 breaks ties by index).
+ * workspace: frr_sort_pairs_workspace_bytes(n) bytes; n < 2^32. */
+size_t frr_sort_pairs_workspace_bytes(int64_t n);
+int frr_sort_pairs(uint64_t* keys, uint64_t* vals, int64_t n, int key_bits, void* workspace, size_t ws_bytes,
+                   void* stream);
+
 /* ---- randomization test (inference.py:82-101, 129-182) ----------------- */
 /* Difference in means of y per assignment with numpy's pairwise reduction
  * order (a), the same for y = obs assignment via popcounts (b), and whether

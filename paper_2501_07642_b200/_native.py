@@ -74,6 +74,8 @@ SIGNATURES = {
     "frr_select_workspace_bytes": (sz, [i64]),
     "frr_select_compact": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
     "frr_select_compact_capped": (i32, [vp, i64, i64, vp, vp, i64, vp, vp, vp, vp, vp]),
+    "frr_sort_pairs_workspace_bytes": (sz, [i64]),
+    "frr_sort_pairs": (i32, [vp, vp, i64, i32, vp, sz, vp]),
     "frr_dim_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_mc_workspace_bytes": (sz, [i64, i32]),
     "frr_dim_mc_ws": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),

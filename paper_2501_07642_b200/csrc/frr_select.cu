@@ -49,22 +49,42 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const uint64_t* __restric
         if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
 }
 
-__global__ void k_pick(const unsigned long long* hist, frr_select_state_t* st, int shift) {
-    if (threadIdx.x != 0) return;
-    int64_t k = st->k_rem;
-    unsigned long long cum = 0;
-    int digit = 255;
-    for (int dgt = 0; dgt < 256; dgt++) {
-        unsigned long long h = hist[dgt];
-        if ((int64_t)(cum + h) >= k) {
-            digit = dgt;
-            break;
-        }
-        cum += h;
+// One warp: lane l owns bins 8l..8l+7; an inclusive warp scan of the lane
+// sums finds the lane holding rank k_rem, that lane its digit.
+__global__ void __launch_bounds__(32) k_pick(const unsigned long long* hist, frr_select_state_t* st, int shift) {
+    const int lane = threadIdx.x;
+    const int64_t k = st->k_rem;
+    unsigned long long h[8], own = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        h[i] = hist[8 * lane + i];
+        own += h[i];
     }
-    st->k_rem = k - (int64_t)cum;
-    st->prefix |= (uint64_t)digit << shift;
-    st->mask |= 255ull << shift;
+    unsigned long long incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(FRR_FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    // k <= total (k_rem counts ranks inside the current prefix): the first
+    // lane whose inclusive sum reaches k holds the digit
+    const unsigned hit = __ballot_sync(FRR_FULL, (int64_t)incl >= k);
+    const int src = hit ? __ffs(hit) - 1 : 31;
+    if (lane == src) {
+        unsigned long long cum = incl - own;
+        int digit = 8 * lane + 7;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            if ((int64_t)(cum + h[i]) >= k) {
+                digit = 8 * lane + i;
+                break;
+            }
+            cum += h[i];
+        }
+        st->k_rem = k - (int64_t)cum;
+        st->prefix |= (uint64_t)digit << shift;
+        st->mask |= 255ull << shift;
+    }
 }
 
 __global__ void k_init(frr_select_state_t* st, int64_t k) {
@@ -332,4 +352,177 @@ extern "C" int frr_select_compact_capped(const double* stats, int64_t m, int64_t
     k_compact<<<(unsigned)ntiles, kCThreads, 0, s>>>(bits, m, index_base, st, tie_quota, ws, cap, idx_out,
                                                      stat_out);
     return frr_launched("k_compact");
+}
+
+// ------------------------------------------------- (key, value) pair sort
+// Stable LSD radix sort of uint64 keys carrying 8-byte values, 8-bit digits:
+// the fused exact pass keeps its (rank, statistic) pairs in arrival order,
+// the select and the pool want them by rank.  Per pass: per-tile digit
+// counts, one exclusive scan over [digit][tile], then a stable scatter --
+// every tile walks its elements in index order, 256 per round, ranking equal
+// digits inside a warp with __match_any_sync and across warps / rounds
+// through shared counters.
+namespace {
+constexpr int kSortThreads = 256, kSortRounds = 8, kSortTile = kSortThreads * kSortRounds;
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                                                            uint32_t* counts, int64_t ntiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; r++) {
+        const int64_t i = base + r * kSortThreads + threadIdx.x;
+        const bool ok = i < n;
+        const unsigned d = ok ? (unsigned)(keys[i] >> shift) & 255u : 0u;
+        const unsigned act = __ballot_sync(FRR_FULL, ok);
+        if (ok) {
+            const unsigned peers = __match_any_sync(act, d);
+            if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// CTA d: exclusive scan of digit d's per-tile counts counts[d][0, ntiles) in
+// place, and the digit's total
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* counts, int64_t ntiles, uint32_t* totals) {
+    __shared__ uint32_t warp_sum[32];
+    __shared__ uint32_t carry;
+    uint32_t* row = counts + (int64_t)blockIdx.x * ntiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < ntiles; c0 += 1024) {
+        const int64_t i = c0 + threadIdx.x;
+        const uint32_t v = i < ntiles ? row[i] : 0u;
+        uint32_t x = v;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FRR_FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = warp_sum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FRR_FULL, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_sum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const uint32_t before = carry + (warp ? warp_sum[warp - 1] : 0u) + x - v;
+        if (i < ntiles) row[i] = before;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* __restrict__ kin,
+                                                               const uint64_t* __restrict__ vin, int64_t n, int shift,
+                                                               const uint32_t* __restrict__ offs, int64_t ntiles,
+                                                               const uint32_t* __restrict__ totals,
+                                                               uint64_t* __restrict__ kout,
+                                                               uint64_t* __restrict__ vout) {
+    constexpr int NW = kSortThreads / 32;
+    __shared__ uint32_t run[256];
+    __shared__ uint32_t wc[NW][256];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {  // digit base: exclusive scan of the digit totals (one per thread)
+        const uint32_t tv = totals[tid];
+        uint32_t x = tv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FRR_FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wc[0][warp] = x;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (int w = 0; w < warp; w++) wb += wc[0][w];
+        __syncthreads();
+        run[tid] = wb + x - tv + offs[(int64_t)tid * ntiles + blockIdx.x];
+    }
+    for (int w = 0; w < NW; w++) wc[w][tid] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortRounds; r++) {
+        const int64_t i = base + r * kSortThreads + tid;
+        const bool ok = i < n;
+        uint64_t k = 0, v = 0;
+        unsigned d = 0, peers = 0;
+        const unsigned act = __ballot_sync(FRR_FULL, ok);
+        if (ok) {
+            k = kin[i];
+            v = vin[i];
+            d = (unsigned)(k >> shift) & 255u;
+            peers = __match_any_sync(act, d);
+            if ((__ffs(peers) - 1) == lane) wc[warp][d] = __popc(peers);
+        }
+        __syncthreads();
+        if (ok) {
+            uint32_t before = run[d] + __popc(peers & ((1u << lane) - 1u));
+            for (int w = 0; w < warp; w++) before += wc[w][d];
+            kout[before] = k;
+            vout[before] = v;
+        }
+        __syncthreads();
+        uint32_t tot = 0;  // thread tid: digit tid's count in this round
+        for (int w = 0; w < NW; w++) {
+            tot += wc[w][tid];
+            wc[w][tid] = 0;
+        }
+        run[tid] += tot;
+        __syncthreads();
+    }
+}
+}  // namespace
+
+extern "C" size_t frr_sort_pairs_workspace_bytes(int64_t n) {
+    const int64_t ntiles = std::max<int64_t>(1, frr_cdiv(n, kSortTile));
+    return (size_t)std::max<int64_t>(n, 1) * 16 + ((size_t)ntiles + 1) * 256 * sizeof(uint32_t);
+}
+
+extern "C" int frr_sort_pairs(uint64_t* keys, uint64_t* vals, int64_t n, int key_bits, void* workspace,
+                              size_t ws_bytes, void* stream) {
+    if (n <= 1) return FRR_OK;
+    if (key_bits < 1 || key_bits > 64 || ws_bytes < frr_sort_pairs_workspace_bytes(n)) {
+        frr_set_error("frr_sort_pairs: key_bits in [1, 64] and frr_sort_pairs_workspace_bytes(n) of workspace");
+        return FRR_E_INVALID_DESIGN;
+    }
+    if (n > 0xFFFFFFFFll) {
+        frr_set_error("frr_sort_pairs: n < 2^32");
+        return FRR_E_UNSUPPORTED;
+    }
+    cudaStream_t s = frr_stream(stream);
+    const int64_t ntiles = frr_cdiv(n, kSortTile);
+    uint64_t* kt = static_cast<uint64_t*>(workspace);
+    uint64_t* vt = kt + n;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(vt + n);
+    uint32_t* totals = counts + (size_t)ntiles * 256;
+    uint64_t *ka = keys, *va = vals, *kb = kt, *vb = vt;
+    const int passes = (key_bits + 7) / 8;
+    int rc;
+    for (int p = 0; p < passes; p++) {
+        k_sort_hist<<<(unsigned)ntiles, kSortThreads, 0, s>>>(ka, n, 8 * p, counts, ntiles);
+        if ((rc = frr_launched("k_sort_hist"))) return rc;
+        k_sort_scan<<<256, 1024, 0, s>>>(counts, ntiles, totals);
+        if ((rc = frr_launched("k_sort_scan"))) return rc;
+        k_sort_scatter<<<(unsigned)ntiles, kSortThreads, 0, s>>>(ka, va, n, 8 * p, counts, ntiles, totals, kb, vb);
+        if ((rc = frr_launched("k_sort_scatter"))) return rc;
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (ka != keys) {  // odd pass count: the result is in the workspace
+        if (cudaMemcpyAsync(keys, ka, (size_t)n * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(vals, va, (size_t)n * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return frr_check_launch("frr_sort_pairs copy");
+    }
+    return FRR_OK;
 }

@@ -78,6 +78,11 @@ def _patch_fused(setattr_, variant):
         idx, val = lo + keep[:cap], st[keep[:cap]]
         return torch.from_numpy(idx.astype(np.int64)), torch.from_numpy(val.copy()), int(keep.size)
 
+    def sort_by_rank(ranks, vals, rank_end):  # checker stand-in for frr_sort_pairs
+        order = np.argsort(ranks.numpy(), kind="stable")
+        return ranks[order].contiguous(), vals[order].contiguous()
+
+    setattr_(G, "_sort_by_rank", sort_by_rank)
     setattr_(G, "_use_fused_select", lambda design, d, m, k: design.mode == "exact")
     setattr_(G, "_narrow_sample", sample)
     setattr_(G, "_narrow_filter", filt)

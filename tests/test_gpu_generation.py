@@ -436,3 +436,31 @@ def test_c4_fused_pool_equals_unfused_full_size(monkeypatch):
     fused, plain = _exact_pool_both(X, design, monkeypatch)
     assert fused.n_accepted == 2_333_606
     assert G.pools_equal(fused, plain) and np.array_equal(fused.assignments, plain.assignments)
+
+
+@pytest.mark.parametrize("n,bits,dups", [(1, 8, False), (2, 1, False), (1000, 8, False), (5000, 20, False),
+                                         (3_000_001, 32, False), (100_000, 40, True), (70_000, 64, True)])
+def test_sort_pairs_vs_stable_argsort(n, bits, dups):
+    """frr_sort_pairs (the fused exact pass's rank ordering) against numpy's
+    stable argsort, odd and even pass counts, duplicate keys keep their
+    input order."""
+    import torch
+
+    from paper_2501_07642_b200 import _native as N
+
+    rng = np.random.default_rng(n + bits)
+    hi = (1 << bits) - 1
+    if dups:
+        keys = rng.integers(0, min(hi, 1000), size=n, dtype=np.uint64, endpoint=True)
+    else:  # distinct keys (like ranks), shuffled
+        keys = rng.permutation(np.unique(rng.integers(0, hi, size=n, dtype=np.uint64, endpoint=True)))
+        n = keys.shape[0]
+    vals = np.arange(n, dtype=np.int64)
+    k_dev = torch.from_numpy(keys.view(np.int64).copy()).cuda()
+    v_dev = torch.from_numpy(vals.copy()).cuda()
+    ws_bytes = int(N.lib().frr_sort_pairs_workspace_bytes(n))
+    ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device="cuda")
+    N.call("frr_sort_pairs", N.ptr(k_dev), N.ptr(v_dev), n, bits, N.ptr(ws), ws_bytes, N.stream_ptr())
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(k_dev.cpu().numpy().view(np.uint64), keys[order])
+    assert np.array_equal(v_dev.cpu().numpy(), vals[order])
