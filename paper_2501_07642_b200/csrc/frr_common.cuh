@@ -151,9 +151,14 @@ __device__ __forceinline__ uint32_t frr_fy_draw(uint64_t x, const StepC* sp, uin
 #define FRR_FY_ROUNDS 4
 #endif
 
+// CLIP: steps k >= t are no-ops whatever their table record says (the
+// universal global step table frr_global_steps has real bounds there; the
+// per-(n, t) tables have b = 1 dummies and need no clipping).
+template <bool CLIP = false>
 __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const StepC* steps,
                                             uint16_t* lw, int lane) {
     constexpr int R = FRR_FY_ROUNDS;
+    static_assert(!CLIP || R == 4, "step clipping is implemented for FRR_FY_ROUNDS == 4");
     frr_table_fill(lw, n, 0, lane);
     __syncwarp();
     uint32_t hmax = 0;
@@ -229,6 +234,7 @@ __device__ __forceinline__ void frr_warp_fy(uint64_t state, int n, int t, const 
 #pragma unroll
         for (int i = 0; i < 4; i++) {
             d[i] = frr_fy_draw(x[i], sp + 32 * i, hmax, z[(2 * i) & 3], z[(2 * i + 1) & 3]);
+            if (CLIP && v0 + 32u * i > (uint32_t)t) d[i] = 0;  // step k = v0 + 32 i - 1 >= t
             x[i] += stride;
         }
         uint32_t any;

@@ -14,6 +14,39 @@
 #include "frr_launch.cuh"
 #include "frr_revfy.cuh"
 
+// ------------------------------------------------ universal step table
+namespace {
+constexpr int kDescSteps = 65536 + 128;
+struct DescSteps {
+    StepC v[kDescSteps];
+    constexpr DescSteps() : v() {
+        for (int i = 0; i < kDescSteps; i++) {
+            const uint32_t b = i < 65535 ? 65536u - (uint32_t)i : 1u;
+            v[i].b = b;
+            v[i].c2 = (uint32_t)((1ull << 32) % b);
+            v[i].M = (~0ull) / b + 1ull;
+        }
+    }
+};
+__device__ const DescSteps g_frr_desc_steps = DescSteps();
+}  // namespace
+
+const StepC* frr_global_steps(int n) {
+    static const StepC* cached[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        void* p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_frr_desc_steps) != cudaSuccess) {
+            frr_check_launch("cudaGetSymbolAddress(step table)");
+            return nullptr;
+        }
+        cached[dev] = static_cast<const StepC*>(p);
+    }
+    return cached[dev] + (65536 - n);
+}
+
 namespace {
 
 constexpr int kWarps = 8;  // warps per CTA of k_exact_small
@@ -73,12 +106,12 @@ __device__ __forceinline__ const StepC* cta_steps(unsigned char*& cursor, const 
 enum Source { SRC_KEYS = 0, SRC_RANKS = 1, SRC_ROWS = 2 };
 
 // Build the candidate table for source SRC.
-template <int SRC>
+template <int SRC, bool GS = false>
 __device__ __forceinline__ void build_table(uint64_t seed, const uint64_t* ids, const int8_t* rows,
                                             int64_t c, int n, int t, const StepC* steps, uint16_t* lw,
                                             int lane) {
     if (SRC == SRC_KEYS) {
-        frr_warp_fy(frr_derive_state(seed, ids[c]), n, t, steps, lw, lane);
+        frr_warp_fy<GS>(frr_derive_state(seed, ids[c]), n, t, steps, lw, lane);
     } else if (SRC == SRC_RANKS) {
         frr_table_fill(lw, n, FRR_CTL, lane);
         __syncwarp();
@@ -126,7 +159,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_regen(uint64_t seed, const uin
     __syncthreads();
     const int words = (n + 31) >> 5;
     for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < m; c += (int64_t)gridDim.x * nw) {
-        build_table<SRC>(seed, ids, nullptr, c, n, t, steps, lw, lane);
+        build_table<SRC, GS>(seed, ids, nullptr, c, n, t, steps, lw, lane);
         if (rows) {
             int8_t* out = rows + (size_t)c * n;
             if ((n & 7) == 0) {
@@ -217,9 +250,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_stats_small(frr_balance_t bal,
     const int64_t* __restrict__ zq = bal.zq;
     for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < count; c += (int64_t)gridDim.x * nw) {
         if (SRC == SRC_KEYS) {
-            frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
+            frr_warp_fy<GS>(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
         } else {
-            build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+            build_table<SRC, GS>(seed, ids, rows, c, n, t, steps, lw, lane);
         }
         int64_t acc[D];
 #pragma unroll
@@ -263,9 +296,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_stats_generic(frr_balance_t ba
     __syncthreads();
     for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < count; c += (int64_t)gridDim.x * nw) {
         if (SRC == SRC_KEYS) {
-            frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
+            frr_warp_fy<GS>(frr_derive_state(seed, lo + (uint64_t)c), n, t, steps, lw, lane);
         } else {
-            build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+            build_table<SRC, GS>(seed, ids, rows, c, n, t, steps, lw, lane);
         }
         for (int j = lane; j < d; j += 32) {
             int64_t acc = 0;
@@ -729,7 +762,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_dim(uint64_t seed, const uint6
     const int words = (n + 31) >> 5;
     const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
     for (int64_t c = (int64_t)blockIdx.x * nw + warp; c < m; c += (int64_t)gridDim.x * nw) {
-        build_table<SRC>(seed, ids, rows, c, n, t, steps, lw, lane);
+        build_table<SRC, GS>(seed, ids, rows, c, n, t, steps, lw, lane);
         // b and membership from packed words
         uint32_t pt = 0, pc = 0;
         bool same = true;

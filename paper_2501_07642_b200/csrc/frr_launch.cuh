@@ -46,27 +46,22 @@ static inline int frr_persistent_grid(K kernel, int threads, size_t smem, int64_
 
 static inline cudaStream_t frr_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-namespace {
-__global__ void k_fill_steps_global(StepC* steps, int n, int t) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < frr_steps_len(t); k += gridDim.x * blockDim.x)
-        steps[k] = frr_make_step(k < t ? n : k + 1, k);
-}
+// The universal step table (frr_gen.cu): record i = frr_make_step(max(1,
+// 65536 - i), .) for i < 65536 + 128, immutable data of the library image --
+// step k of any design n is record 65536 - n + k, so one table serves every
+// (n, t) without allocation.  Records k >= t carry real bounds, so its users
+// clip those steps (frr_warp_fy<true>).
+const StepC* frr_global_steps(int n);
 
-// Step table in global memory for the large-t plans (stream-ordered scratch).
+namespace {
+// Step table in global memory for the large-t plans: a view into the
+// universal table (no allocation).
 struct GlobalSteps {
-    StepC* p = nullptr;
-    cudaStream_t s;
-    int init(int n, int t, cudaStream_t st) {
-        s = st;
-        if (cudaMallocAsync((void**)&p, (size_t)frr_steps_len(t) * sizeof(StepC), s) != cudaSuccess)
-            return frr_check_launch("cudaMallocAsync(steps)");
-        k_fill_steps_global<<<std::max(1, frr_steps_len(t) / 256), 256, 0, s>>>(p, n, t);
-        return frr_launched("k_fill_steps_global");
-    }
-    ~GlobalSteps() {
-        if (p) cudaFreeAsync(p, s);
+    const StepC* p = nullptr;
+    int init(int n, int /*t*/, cudaStream_t /*s*/) {
+        p = frr_global_steps(n);
+        return p ? FRR_OK : FRR_E_CUDA;
     }
 };
 
 }  // namespace
-

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int64_t c = tile * BM + r;
                 uint32_t* row = tb + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
                 if (c < count && !(FRR_NT_DEBUG & 8)) {
-                    frr_warp_fy(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
+                    frr_warp_fy<true>(frr_derive_state(seed, lo + (uint64_t)c), S.n, S.t, steps, lw, lane);
                     // control bits in natural unit order, one ballot per word
                     for (int w = 0; w < S.kw; w++) {
                         const int e = 32 * w + lane;
