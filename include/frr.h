@@ -237,6 +237,15 @@ int frr_dim_rows(const int8_t* rows, int64_t m, int n, int t, const double* y,
 int frr_tau_counts(const double* a, const double* b, int64_t m, const double* taus,
                    const double* rhs, int ntau, uint64_t* counts, void* stream);
 
+/* ---- synthetic inputs (reference bench.py:101-154) --------------------- */
+/* Polar-method candidate pairs [pair_lo, pair_lo + npairs) of simulation
+ * stream `stream_id` of root_seed: v1, v2 in [-1, 1) and s = v1^2 + v2^2,
+ * bit-identical to the reference's numpy arithmetic.  The caller keeps the
+ * pairs with 0 < s < 1 and scales them by sqrt(-2 ln s / s) (numpy, so the
+ * logarithm is the reference's own). */
+int frr_sim_pairs(uint64_t root_seed, uint64_t stream_id, int64_t pair_lo, int64_t npairs, double* v1,
+                  double* v2, double* s, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------ */
 /* Thread-per-candidate generator (reverse-bitset Fisher-Yates) on its own:
  * draws [draw_lo, draw_lo+count) -> CONTROL bitsets bits [count, ceil(n/32)]

@@ -87,6 +87,7 @@ SIGNATURES = {
     "frr_microbench_mma_i8": (i32, [i32, i32, i64, vp, vp]),
     "frr_rev_bits": (i32, [u64, u64, i64, i32, i32, vp, vp, vp]),
     "frr_launch_count": (ctypes.c_ulonglong, []),
+    "frr_sim_pairs": (i32, [u64, u64, i64, i64, vp, vp, vp, vp]),
 }
 
 _lock = threading.Lock()

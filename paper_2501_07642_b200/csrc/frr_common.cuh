@@ -56,6 +56,29 @@ __device__ __forceinline__ uint64_t frr_mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// z ^ (z >> s) (0 < s < 32) with the high word's shift on the FMA pipe
+// (hi >> s = umulhi(hi, 2^(32-s))) instead of the ALU pipe
+template <int S>
+__device__ __forceinline__ uint64_t frr_xorshift_fma(uint64_t z) {
+    uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+    const uint32_t lo_s = __funnelshift_r(lo, hi, S);
+    uint32_t hi_s;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi_s) : "r"(hi), "n"(1u << (32 - S)));
+    return ((uint64_t)(hi ^ hi_s) << 32) | (lo ^ lo_s);
+}
+
+// mix64 with a chosen subset of the three xorshifts' high-word shifts on the
+// FMA pipe (bit i of FMA_MASK: xorshift i), balancing the generator's ALU
+// and FMA pipes
+template <int FMA_MASK>
+__device__ __forceinline__ uint64_t frr_mix64_bal(uint64_t z) {
+    z = (FMA_MASK & 1) ? frr_xorshift_fma<30>(z) : z ^ (z >> 30);
+    z = frr_mul64c(z, 0x1CE4E5B9u, 0xBF58476Du);
+    z = (FMA_MASK & 2) ? frr_xorshift_fma<27>(z) : z ^ (z >> 27);
+    z = frr_mul64c(z, 0x133111EBu, 0x94D049BBu);
+    return (FMA_MASK & 4) ? frr_xorshift_fma<31>(z) : z ^ (z >> 31);
+}
+
 // keys.py:118-121
 __device__ __forceinline__ uint64_t frr_derive_state(uint64_t seed, uint64_t draw) {
     return frr_mix64((seed ^ (draw * FRR_GOLDEN)) + FRR_GOLDEN);

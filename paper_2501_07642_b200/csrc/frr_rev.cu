@@ -143,3 +143,39 @@ extern "C" int frr_rev_bits(uint64_t root_seed, uint64_t draw_lo, int64_t count,
                             unsigned long long* sink, void* stream) {
     return rev_launch(root_seed, nullptr, draw_lo, count, n, t, bits, 0, sink, nullptr, stream);
 }
+
+// ------------------------------------------------- simulation streams
+// Polar-method candidates of a keyed simulation stream (reference
+// bench.py:101-136): pair p = stream outputs 2p, 2p+1, output i =
+// mix64(state + (i+1) C) of key (seed, 2^63 + stream); v = 2 (u >> 11) 2^-53 - 1
+// (exact), s = v1 v1 + v2 v2 with numpy's separate roundings.
+namespace {
+__global__ void k_sim_pairs(uint64_t state, int64_t pair_lo, int64_t npairs, double* __restrict__ v1,
+                            double* __restrict__ v2, double* __restrict__ s) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = 2 * (uint64_t)(pair_lo + p) + 1;
+        const uint64_t u1 = frr_mix64(state + i * FRR_GOLDEN), u2 = frr_mix64(state + (i + 1) * FRR_GOLDEN);
+        const double a = __dsub_rn(__dmul_rn(2.0, __dmul_rn((double)(u1 >> 11), 0x1p-53)), 1.0);
+        const double b = __dsub_rn(__dmul_rn(2.0, __dmul_rn((double)(u2 >> 11), 0x1p-53)), 1.0);
+        v1[p] = a;
+        v2[p] = b;
+        s[p] = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+    }
+}
+}  // namespace
+
+extern "C" int frr_sim_pairs(uint64_t root_seed, uint64_t stream_id, int64_t pair_lo, int64_t npairs, double* v1,
+                             double* v2, double* s, void* stream) {
+    if (npairs <= 0) return FRR_OK;
+    const uint64_t state = [&] {
+        // derive_state(AssignmentKey(seed, 2^63 + stream)) (keys.py:118-121)
+        const uint64_t draw = (1ull << 63) + stream_id;
+        uint64_t z = (root_seed ^ (draw * FRR_GOLDEN)) + FRR_GOLDEN;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }();
+    const int grid = (int)std::min<int64_t>(frr_cdiv(npairs, 256), (int64_t)frr_num_sms() * 8);
+    k_sim_pairs<<<grid, 256, 0, frr_stream(stream)>>>(state, pair_lo, npairs, v1, v2, s);
+    return frr_launched("k_sim_pairs");
+}

@@ -30,6 +30,9 @@
 #ifndef FRR_REV_GROUP
 #define FRR_REV_GROUP 8  // draws computed ahead of their bit moves (divides 32)
 #endif
+#ifndef FRR_REV_FMA_MASK
+#define FRR_REV_FMA_MASK 0  // xorshifts whose high-word shift runs on the FMA pipe (frr_mix64_bal)
+#endif
 #ifndef FRR_REV_PIPE
 #define FRR_REV_PIPE 0  // 1: draws of the next group issued ahead of the current group's bit moves (measured: no gain, 2x registers)
 #endif
@@ -121,7 +124,7 @@ __device__ __forceinline__ void frr_rev_draws(uint64_t& x, uint64_t sa, uint32_t
     for (int i = 0; i < FRR_REV_GROUP; i++) {
         x -= FRR_GOLDEN;
         const StepC s = GS ? frr_ldg_step(sa - 16ull * (uint64_t)i) : frr_lds_step((uint32_t)sa - 16u * (uint32_t)i);
-        const uint64_t u = frr_mix64(x);
+        const uint64_t u = frr_mix64_bal<FRR_REV_FMA_MASK>(x);
         hh[i] = (uint32_t)(u >> 32);
         dd[i] = frr_mod_step(u, s, z0, z1);
         FRR_CHECK(dd[i] < s.b && dd[i] == (uint32_t)(u % s.b));

@@ -3,12 +3,15 @@ normal stream, ``simulate_data`` and the accelerator cost model
 (reference bench.py:43-154).
 
 These produce *inputs* for the hot path (covariates, outcomes, the observed
-assignment); they are host-side numpy, bit-identical to the reference on the
-same machine, and not part of the GPU path.  The observed assignment is
-regenerated from its key on the GPU like any other candidate.  The
-reference's timing harness (``run_benchmark`` / ``summarize_benchmark``,
-which times its own naive/batched/parallel CPU paths) is out of scope: this
-package's measurement is ``bench.py``.
+assignment).  The keyed streams and the polar-method candidate pairs are
+computed on the GPU (frr_sim_pairs: splitmix64 outputs, uniforms and
+s = v1^2 + v2^2 in the reference's exact arithmetic); the accepted pairs'
+scale sqrt(-2 ln s / s) is numpy's, so the normals are bit-identical to the
+reference's on the same machine (its logarithm is numpy's).  The observed
+assignment is regenerated from its key on the GPU like any other
+candidate.  The reference's timing harness (``run_benchmark`` /
+``summarize_benchmark``, which times its own naive/batched/parallel CPU
+paths) is out of scope: this package's measurement is ``bench.py``.
 """
 
 from __future__ import annotations
@@ -81,22 +84,17 @@ def estimate_speedup(model: CostModel) -> float:
     return (model.r_cpu + work) / denom
 
 
-def _mix64_array(z: np.ndarray) -> np.ndarray:
-    with np.errstate(over="ignore"):
-        z = z ^ (z >> np.uint64(30))
-        z = z * np.uint64(keymod._M1)
-        z = z ^ (z >> np.uint64(27))
-        z = z * np.uint64(keymod._M2)
-        return z ^ (z >> np.uint64(31))
+def _polar_pairs(seed: int, stream: int, pair_lo: int, npairs: int):
+    """(v1, v2, s) of polar-method pairs [pair_lo, pair_lo + npairs) of a
+    simulation stream, on the GPU (frr_sim_pairs), returned to the host."""
+    from . import _native as N
 
-
-def _stream(seed: int, stream: int, start: int, count: int) -> np.ndarray:
-    """Outputs [start, start+count) of simulation stream `stream`: the
-    counter form mix64(state + (i+1) C) of key (seed, 2^63 + stream)."""
-    state = keymod.derive_state(keymod.AssignmentKey(seed, SIM_STREAM_BASE + stream))
-    i = np.arange(start + 1, start + count + 1, dtype=np.uint64)
-    with np.errstate(over="ignore"):
-        return _mix64_array(np.uint64(state) + i * np.uint64(keymod.GOLDEN))
+    torch = N.torch_mod()
+    out = torch.empty((3, npairs), dtype=torch.float64, device=N.device())
+    N.call("frr_sim_pairs", N.ctypes.c_uint64(int(seed) & keymod.MASK64), N.ctypes.c_uint64(int(stream)), pair_lo,
+           npairs, N.ptr(out[0]), N.ptr(out[1]), N.ptr(out[2]), N.stream_ptr())
+    h = out.cpu().numpy()
+    return h[0], h[1], h[2]
 
 
 def normals_from_stream(seed: int, stream: int, count: int) -> np.ndarray:
@@ -110,10 +108,7 @@ def normals_from_stream(seed: int, stream: int, count: int) -> np.ndarray:
     while filled < count:
         want = (count - filled + 1) // 2
         take = max(64, int(1.3 * want) + 16)  # ~21% of pairs are rejected
-        u = _stream(seed, stream, 2 * pair, 2 * take)
-        v = 2.0 * ((u >> np.uint64(11)).astype(np.float64) * (2.0**-53)) - 1.0
-        v1, v2 = v[0::2], v[1::2]
-        s = v1 * v1 + v2 * v2
+        v1, v2, s = _polar_pairs(seed, stream, pair, take)
         ok = (s > 0.0) & (s < 1.0)
         g = np.sqrt(-2.0 * np.log(s[ok]) / s[ok])
         z = np.empty(2 * int(ok.sum()), dtype=np.float64)
