@@ -151,14 +151,17 @@ template <bool GS = false>
 __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps, uint32_t wsa, int kw) {
     constexpr int GPW = 32 / FRR_REV_GROUP;  // groups per 32-step word block
     const int wtop = (t - 1) >> 5;
+    // whole groups of the top word above step t - 1 are dummies: skipped
+    const int q0 = (31 - ((t - 1) & 31)) / FRR_REV_GROUP;
     frr_rev_fill(wsa, wtop + 1, kw);
     uint32_t hmax = 0;
     // zeros opaque to the compiler: the high words of frr_mod_step's 64-bit
     // addends stay live instead of being re-zeroed every draw
     uint32_t z0 = (uint32_t)t >> 31, z1 = (uint32_t)(t + 1) >> 31;
-    // x = state + (j + 1) C for the step j about to be drawn
-    uint64_t x = state + (uint64_t)(32 * wtop + 33) * FRR_GOLDEN;
-    uint64_t sa = steps + 16ull * (uint64_t)(32 * wtop + 31);  // record of the next step to draw
+    // x = state + (j + 1) C for the step j about to be drawn; sa = its record
+    const int j0 = 32 * wtop + 31 - FRR_REV_GROUP * q0;
+    uint64_t x = state + (uint64_t)(j0 + 2) * FRR_GOLDEN;
+    uint64_t sa = steps + 16ull * (uint64_t)j0;
     uint32_t dn[FRR_REV_GROUP];
     frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
     sa -= 16ull * FRR_REV_GROUP;
@@ -170,6 +173,7 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(init) : "memory");
 #pragma unroll
         for (int q = 0; q < GPW; q++) {
+            if (W == wtop && q < q0) continue;
             uint32_t dd[FRR_REV_GROUP];
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) dd[i] = dn[i];
