@@ -57,6 +57,9 @@ class ClockSampler:
         self.samples = []
         self.proc = None
 
+    # Sampling every 500 ms: each NVML query can stall this process's CUDA
+    # calls for tens of ms (measured at 200 ms: 10% of the step time lost to
+    # stalls of the select's host syncs; 500 ms: 0.5%, no sampling: 0).
     # nvidia-smi writes to a temporary file that is parsed after the timed
     # region: a reader thread in this interpreter would contend for the GIL
     # with the step's host orchestration and show up as ~5% step time.
@@ -70,7 +73,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", os.environ.get("FRR_CLOCK_MS", "200")], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("FRR_CLOCK_MS", "500")], stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         # let nvidia-smi finish its NVML start-up before the timed region:
