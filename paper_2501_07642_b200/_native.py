@@ -179,46 +179,64 @@ def _stage_ring():
 
 
 def to_host(t):
-    """Device tensor -> numpy array (a fresh, caller-owned array).  Large
-    results (accepted indices, statistics, assignment rows) stream through a
-    fixed ring of page-locked staging slots: the DMA of chunk i + 1 overlaps
-    the host copy of chunk i out of its slot, and a slot is reused once its
-    host copy has finished (a pageable .cpu() of the 79 MB C4 row matrix
-    runs at ~2 GB/s).  No page-locked memory is handed to callers and the
-    staging footprint does not grow with the result."""
+    """Device tensor -> numpy array (a fresh, caller-owned array); see to_host_many."""
+    return to_host_many(t)[0]
+
+
+def to_host_many(*tensors):
+    """Device tensors -> fresh, caller-owned numpy arrays.  Large results
+    (accepted indices, statistics, assignment rows) stream through a fixed
+    ring of page-locked staging slots, all tensors in one pipeline: the DMA
+    of chunk i + 1 overlaps the host copy of chunk i out of its slot, and a
+    slot is reused once its host copy has finished (a pageable .cpu() of the
+    79 MB C4 row matrix runs at ~2 GB/s).  No page-locked memory is handed to
+    callers and the staging footprint does not grow with the result."""
     torch = torch_mod()
-    nbytes = t.numel() * t.element_size()
-    if not t.is_cuda or nbytes < STAGE_MIN_BYTES:
-        return t.cpu().numpy()
     import numpy as np
+
+    outs = [None] * len(tensors)
+    big = []
+    for i, t in enumerate(tensors):
+        nbytes = t.numel() * t.element_size()
+        if not t.is_cuda or nbytes < STAGE_MIN_BYTES:
+            outs[i] = t.cpu().numpy()
+        else:
+            big.append(i)
+    if not big:
+        return outs
     from concurrent.futures import ThreadPoolExecutor
 
-    t = t.contiguous()
-    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
-    dst = out.reshape(-1).view(np.uint8)
     with _stage_lock:
         ring = _stage_ring()
-        flat = t.reshape(-1).view(torch.uint8)
-        stream = torch.cuda.current_stream(t.device)
         if _stage["pool"] is None:
             # host copies of different slots run in parallel (np.copyto drops the GIL)
             _stage["pool"] = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)))
         pending = [None] * STAGE_SLOTS  # host-copy future per slot
 
-        def land(slot, a, n, ev):
+        def land(slot, dst, a, n, ev):
             ev.synchronize()
             np.copyto(dst[a:a + n], ring[slot].numpy()[:n])
 
-        for i, a in enumerate(range(0, nbytes, STAGE_CHUNK)):
-            slot = i % STAGE_SLOTS
-            if pending[slot] is not None:
-                pending[slot].result()  # the slot's previous chunk has left it
-            n = min(STAGE_CHUNK, nbytes - a)
-            ring[slot][:n].copy_(flat[a:a + n], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            pending[slot] = _stage["pool"].submit(land, slot, a, n, ev)
+        k = 0
+        for i in big:
+            t = tensors[i].contiguous()
+            out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+            outs[i] = out
+            dst = out.reshape(-1).view(np.uint8)
+            flat = t.reshape(-1).view(torch.uint8)
+            nbytes = flat.numel()
+            stream = torch.cuda.current_stream(t.device)
+            for a in range(0, nbytes, STAGE_CHUNK):
+                slot = k % STAGE_SLOTS
+                k += 1
+                if pending[slot] is not None:
+                    pending[slot].result()  # the slot's previous chunk has left it
+                n = min(STAGE_CHUNK, nbytes - a)
+                ring[slot][:n].copy_(flat[a:a + n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                pending[slot] = _stage["pool"].submit(land, slot, dst, a, n, ev)
         for f in pending:
             if f is not None:
                 f.result()
-    return out
+    return outs
