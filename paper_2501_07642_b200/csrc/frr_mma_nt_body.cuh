@@ -16,8 +16,17 @@ constexpr int KC = FRR_NT_KC;  // K bytes per stage: this instantiation's (128 o
 #endif
 // thread-per-candidate generators (frr_rev_fy): at most RFY warps (a
 // multiple of 4: one tile in flight per 4) and MAXB tile buffers
+// epilogue limb recombination through the unrolled 32-bit pair helper
+#ifndef FRR_NT_PAIRS
+#define FRR_NT_PAIRS 0  // measured slower than tc_limbs8 (runtime limb loop) in this kernel
+#endif
+// epilogue warps per TMEM lane quadrant: 2 splits each 8-column group (the
+// accumulator streams r0..r3 / r4..r7 of numpy's pairwise leaves), 1 = whole
+#ifndef FRR_NT_EPIW
+#define FRR_NT_EPIW 2
+#endif
 #ifndef FRR_NT_RFY
-#define FRR_NT_RFY 16
+#define FRR_NT_RFY (FRR_NT_EPIW == 2 ? 12 : 16)
 #endif
 #ifndef FRR_NT_MAXB
 #define FRR_NT_MAXB 8
@@ -51,6 +60,8 @@ __device__ unsigned long long g_nt_waits[16];
 constexpr int NST = KC == 256 ? 2 : FRR_NT_ST;  // TMEM holds two 64-column A stages at KC = 256
 constexpr int NFY = FRR_NT_NFY;
 constexpr int RFY = FRR_NT_RFY;
+constexpr int EPIW = FRR_NT_EPIW;
+static_assert(EPIW == 1 || EPIW == 2, "epilogue warps per quadrant");
 constexpr int MAXB = FRR_NT_MAXB;
 constexpr int NEXP = FRR_NT_NEXP;          // expansion warps (4 or 8: 1 or 2 threads per row)
 // Warp roles (the scheduler favours higher warp ids; the epilogue is the
@@ -65,7 +76,7 @@ constexpr int W_EXP0 = 0, W_FY0 = NEXP;
 __host__ __device__ constexpr int w_tma(int nfy) { return W_FY0 + nfy; }
 __host__ __device__ constexpr int w_mma(int nfy) { return W_FY0 + nfy + 1; }
 __host__ __device__ constexpr int w_epi0(int nfy) { return (W_FY0 + nfy + 2 + 3) & ~3; }
-__host__ __device__ constexpr int n_warps(int nfy) { return w_epi0(nfy) + 4; }
+__host__ __device__ constexpr int n_warps(int nfy) { return w_epi0(nfy) + 4 * EPIW; }
 #elif FRR_NT_LAYOUT == 1
 constexpr int W_EXP0 = 4, W_FY0 = W_EXP0 + NEXP;
 __host__ __device__ constexpr int w_tma(int nfy) { return W_FY0 + nfy; }
@@ -91,7 +102,7 @@ struct NtShape {
 };
 
 struct NtPlan {
-    size_t a, b, bits, steps, tables, starts, ncomb, bars, total;
+    size_t a, b, bits, steps, tables, starts, ncomb, xch, bars, total;
 };
 
 // tile buffer: 128 bit rows of kw words, [row / 32][word][row % 32] (see
@@ -121,6 +132,8 @@ __host__ __device__ inline NtPlan nt_plan(const NtShape& s) {
     p.ncomb = o;
     o += MAX_LEAVES;
     o = up(o, 16);
+    p.xch = o;  // split epilogue: half-leaf sums handed between a quadrant's warps
+    o += (EPIW == 2 ? 2 * BM * sizeof(double) : 0);
     p.bars = o;
     o += 32 * 8 + 16;  // barriers: also the FRR_TABLE_SLACK after the tables
     static_assert(32 * 8 + 16 >= FRR_TABLE_SLACK, "table slack");
@@ -216,6 +229,47 @@ __device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
 #endif
 }
 
+__device__ __forceinline__ void tc_ld4(uint32_t taddr, int32_t (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// exact S of 4 consecutive columns from L limbs (column l*stride + u), as tc_limbs8
+__device__ __forceinline__ void tc_limbs4(uint32_t base, int L, int stride, bool pair32, int64_t (&Sj)[4]) {
+    int l = L - 1;
+    if (pair32 && !(L & 1)) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) Sj[u] = 0;
+    } else {
+        int32_t v[4];
+        tc_ld4(base + (uint32_t)(l * stride), v);
+        tc_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; u++) Sj[u] = v[u];
+        l--;
+    }
+    if (pair32) {
+        for (; l > 0; l -= 2) {
+            int32_t vh[4], vl[4];
+            tc_ld4(base + (uint32_t)(l * stride), vh);
+            tc_ld4(base + (uint32_t)((l - 1) * stride), vl);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 65536 + (int64_t)(vh[u] * 256 + vl[u]);
+        }
+    } else {
+        for (; l >= 0; l--) {
+            int32_t v[4];
+            tc_ld4(base + (uint32_t)(l * stride), v);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 256 + v[u];
+        }
+    }
+}
+
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
     return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -267,7 +321,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(&bars[B_TM_FULL + s], 1);
-            mbar_init(&bars[B_TM_EMPTY + s], 4);
+            mbar_init(&bars[B_TM_EMPTY + s], 4 * EPIW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -389,7 +443,120 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars[B_BITS_EMPTY + buf]);
         }
-    } else if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
+    } else if (EPIW == 2 && warp >= W_EPI0 && warp < W_EPI0 + 8) {
+        // ================================== streaming epilogue, two warps per quadrant
+        // Warp half h of quadrant q owns columns 4h..4h+3 of every 8-column group,
+        // i.e. numpy's accumulator streams r_{4h..4h+3} of each pairwise leaf.
+        // A leaf's combination ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) joins the
+        // halves through shared memory; half 0 keeps the combine stack.  The
+        // tail group of d % 8 columns is loaded whole by half 0.
+        const int k = warp - W_EPI0, quad = k & 3, half = k >> 2;
+        const int r = quad * 32 + lane;  // tile row == TMEM lane
+        const uint32_t tl = tmem_base + ((uint32_t)(quad * 32) << 16);
+        double* xch = reinterpret_cast<double*>(smem + P.xch);  // [parity][row]
+        const double g = bal.g, cst = bal.cst;
+        const int d = S.d;
+        const bool pair32 = (int64_t)S.n * (128 << 3) * 257 < (1ll << 31);
+        uint32_t chunk_ctr = 0, xphase = 0;
+        // the two warps of a quadrant meet at named barrier 1 + quad
+        auto meet = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory"); };
+        // joins the halves of the open leaf; half 0 returns the leaf sum
+        auto join = [&](const double (&ra)[4]) -> double {
+            const double part = __dadd_rn(__dadd_rn(ra[0], ra[1]), __dadd_rn(ra[2], ra[3]));
+            double* slot = xch + (xphase & 1) * BM + r;
+            if (half == 1) *slot = part;
+            meet();
+            xphase++;
+            return half == 0 ? __dadd_rn(part, *slot) : 0.0;
+        };
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            double racc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) racc[u] = 0.0;
+            double stk[16];
+            int sp = 0, leaf = -1;
+            bool done = false;
+            for (int c = 0; c < S.nch; c++, chunk_ctr++) {
+                const int tb = chunk_ctr & 1;
+                NTW(3, mbar_wait_lazy(&bars[B_TM_FULL + tb], (chunk_ctr >> 1) & 1));
+                tc_fence_after();
+                const uint32_t cb = tl + (uint32_t)(tb * S.nc);
+                for (int g4 = 0; g4 < DJ / 8; g4++) {
+                    if (FRR_NT_DEBUG & 4) break;
+                    const int j0 = c * DJ + g4 * 8;
+                    if (j0 >= d) break;
+                    const int G = j0 >> 3;
+                    const bool starts_leaf = (starts[G >> 5] >> (G & 31)) & 1u;
+                    if (!starts_leaf && j0 + 8 > d) {
+                        // tail of the last leaf: combine, then add the tail columns in order
+                        const double res0 = join(racc);
+                        if (half == 0) {
+                            int64_t Sj[8];
+                            tc_limbs8(cb + (uint32_t)(g4 * 8), S.L, DJ, pair32, Sj);
+                            double res = res0;
+#pragma unroll
+                            for (int u = 0; u < 8; u++)
+                                if (j0 + u < d) {
+                                    const double delta =
+                                        __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> 3), g), bal.cc[j0 + u]);
+                                    res = __dadd_rn(res, __dmul_rn(delta, delta));
+                                }
+                            stk[sp++] = res;
+                            for (int m = ncomb[leaf]; m > 0; m--) {
+                                sp--;
+                                stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                            }
+                        }
+                        done = true;
+                        continue;
+                    }
+                    int64_t Sj[4];
+                    tc_limbs4(cb + (uint32_t)(g4 * 8 + 4 * half), S.L, DJ, pair32, Sj);
+                    double q[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int j = j0 + 4 * half + u;
+                        const double delta =
+                            __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u] >> 3), g), j < d ? bal.cc[j] : 0.0);
+                        q[u] = __dmul_rn(delta, delta);
+                    }
+                    if (starts_leaf) {
+                        if (leaf >= 0) {  // close the previous leaf
+                            const double lv = join(racc);
+                            if (half == 0) {
+                                stk[sp++] = lv;
+                                for (int m = ncomb[leaf]; m > 0; m--) {
+                                    sp--;
+                                    stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                                }
+                            }
+                        }
+                        leaf++;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) racc[u] = q[u];
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) racc[u] = __dadd_rn(racc[u], q[u]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[B_TM_EMPTY + tb]);
+            }
+            if (!done) {
+                const double lv = join(racc);
+                if (half == 0) {
+                    stk[sp++] = lv;
+                    for (int m = ncomb[leaf]; m > 0; m--) {
+                        sp--;
+                        stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]);
+                    }
+                }
+            }
+            const int64_t cidx = tile * BM + r;
+            if (half == 0 && cidx < count) out[cidx] = __dmul_rn(__dadd_rn(0.0, stk[0]), cst);
+        }
+    } else if (EPIW == 1 && warp >= W_EPI0 && warp < W_EPI0 + 4) {
         // ================================================ streaming epilogue
         const int r = threadIdx.x - W_EPI0 * 32;  // tile row == TMEM lane
         const uint32_t tl = tmem_base + ((uint32_t)((warp - W_EPI0) * 32) << 16);
@@ -416,7 +583,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (j0 >= d) break;
                     int64_t Sj[8];
                     const uint32_t cg = cb + (uint32_t)(g4 * 8);
-                    tc_limbs8(cg, S.L, DJ, pair32, Sj);
+#if FRR_NT_PAIRS
+                    if (pair32)
+                        tc_limbs8_fast(cg, S.L, DJ, Sj);
+                    else
+#endif
+                        tc_limbs8(cg, S.L, DJ, pair32, Sj);
                     double q[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
@@ -534,7 +706,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #if FRR_NT_TIMING
     {
         const int role = warp == W_MMA ? 11 : warp == W_TMA ? 12
-                       : warp >= W_EPI0 && warp < W_EPI0 + 4 ? 10
+                       : warp >= W_EPI0 && warp < W_EPI0 + 4 * EPIW ? 10
                        : warp >= W_EXP0 && warp < W_EXP0 + NEXP ? 9 : 8;
         wacc[role] += clock64() - tstart;
         if (lane == 0)

@@ -34,7 +34,7 @@
 #define FRR_REV_FMA_MASK 0  // xorshifts whose high-word shift runs on the FMA pipe (frr_mix64_bal)
 #endif
 #ifndef FRR_REV_PIPE
-#define FRR_REV_PIPE 0  // 1: draws of the next group issued ahead of the current group's bit moves (measured: no gain, 2x registers)
+#define FRR_REV_PIPE 0  // 1: next group's draws ahead of the bit moves; 2: interleaved draw/move
 #endif
 #ifndef FRR_REV_FETCH_AND
 #define FRR_REV_FETCH_AND 1  // 1: atom.and fetch-and-clear for the r-side bit
@@ -70,6 +70,18 @@ __device__ __forceinline__ StepC frr_ldg_step(uint64_t a) {
 // initial set; padding beyond n stays control, its operand rows are zero)
 __device__ __forceinline__ void frr_rev_fill(uint32_t wsa, int from, int to) {
     for (int w = from; w < to; w++) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wsa + 128u * (uint32_t)w), "r"(~0u) : "memory");
+}
+
+// One draw of the group (step record at sa): d and hi(u).
+template <bool GS>
+__device__ __forceinline__ uint32_t frr_rev_draw1(uint64_t& x, uint64_t sa, uint32_t z0, uint32_t z1, uint32_t& h) {
+    x -= FRR_GOLDEN;
+    const StepC s = GS ? frr_ldg_step(sa) : frr_lds_step((uint32_t)sa);
+    const uint64_t u = frr_mix64_bal<FRR_REV_FMA_MASK>(x);
+    h = (uint32_t)(u >> 32);
+    const uint32_t d = frr_mod_step(u, s, z0, z1);
+    FRR_CHECK(d < s.b && d == (uint32_t)(u % s.b));
+    return d;
 }
 
 // Builds the control bitset of candidate `state` into this lane's column of
@@ -177,9 +189,27 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps
             uint32_t dd[FRR_REV_GROUP];
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) dd[i] = dn[i];
-            if (FRR_REV_PIPE && (q < GPW - 1 || W > 0)) {  // the next group (the last one has none)
+            if (FRR_REV_PIPE == 1 && (q < GPW - 1 || W > 0)) {  // the next group (the last one has none)
                 frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
                 sa -= 16ull * FRR_REV_GROUP;
+            }
+            if (FRR_REV_PIPE == 2) {
+                // interleaved: the next group's draw i fills the latency of
+                // this group's bit move i (each move waits for its atomic)
+                const bool more = q < GPW - 1 || W > 0;
+                uint32_t hh[FRR_REV_GROUP];
+#pragma unroll
+                for (int i = 0; i < FRR_REV_GROUP; i++) {
+                    const int jb = 31 - q * FRR_REV_GROUP - i;
+                    FRR_CHECK(32 * W + jb + (int)dd[i] < 32 * kw);  // r inside this lane's bitset
+                    frr_rev_move(wa, (uint32_t)jb + dd[i], dd[i]);
+                    hh[i] = 0;
+                    if (more) dn[i] = frr_rev_draw1<GS>(x, sa - 16ull * (uint64_t)i, z0, z1, hh[i]);
+                }
+#pragma unroll
+                for (int i = 0; i + 1 < FRR_REV_GROUP; i += 2) hmax = max(hmax, max(hh[i], hh[i + 1]));
+                if (more) sa -= 16ull * FRR_REV_GROUP;
+                continue;
             }
 #pragma unroll
             for (int i = 0; i < FRR_REV_GROUP; i++) {
