@@ -31,8 +31,11 @@ namespace {
 using namespace frr_tc;
 
 constexpr int BM = 128;        // candidates per tile = MMA M
+#ifndef FRR_MMA_TW
+#define FRR_MMA_TW 1  // 2 measured -2% (20 generators + 8 tile warps vs 24 + 4)
+#endif
 #ifndef FRR_MMA_NFY
-#define FRR_MMA_NFY 26
+#define FRR_MMA_NFY (FRR_MMA_TW == 2 ? 20 : 26)
 #endif
 #ifndef FRR_MMA_KC
 #define FRR_MMA_KC 64
@@ -57,13 +60,19 @@ constexpr int B_STAGES = FRR_MMA_STAGES;
 constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: their tables share smem)
 // thread-per-candidate generators: RFY warps (4 per tile in flight, a
 // multiple of 4) building rows in place in RBITS tile buffers
+// tile warps per TMEM lane quadrant (FRR_MMA_TW, above): 2 split each
+// tile's expansion (K chunks by parity) and epilogue (columns 0-3 / 4-7 of
+// every 8-group: numpy's accumulator streams r0-3 / r4-7, joined through
+// shared memory)
 #ifndef FRR_MMA_RFY
-#define FRR_MMA_RFY 24
+#define FRR_MMA_RFY (FRR_MMA_TW == 2 ? 20 : 24)
 #endif
 #ifndef FRR_MMA_RBITS
 #define FRR_MMA_RBITS 8
 #endif
 constexpr int RFY = FRR_MMA_RFY;
+constexpr int TW2 = FRR_MMA_TW;
+static_assert(TW2 == 1 || TW2 == 2, "tile warps per quadrant");
 constexpr int RBITS = FRR_MMA_RBITS;
 constexpr int MAXBITS = NBITS > RBITS ? NBITS : RBITS;
 // Wait-time accounting (debug builds only): per-slot clock64 sums read back
@@ -98,8 +107,9 @@ __device__ unsigned long long g_frr_waits[16];
 // copy and MMA warps, then the 4 tile warps at a multiple of 4 (warp % 4 is
 // their TMEM lane quadrant).  The scheduler favours higher warp ids, so the
 // latency-critical roles sit above the generators.
-constexpr int NTHREADS_MAX = ((((NFY > RFY ? NFY : RFY) + 2 + 3) & ~3) + 4) * 32;
+constexpr int NTHREADS_MAX = ((((NFY > RFY ? NFY : RFY) + 2 + 3) & ~3) + 4 * TW2) * 32;
 constexpr int NTHREADS = NTHREADS_MAX;  // launch bound: the largest layout
+static_assert(NTHREADS <= 1024, "roles exceed one CTA (FRR_MMA_TW=2 needs FRR_MMA_NFY <= 20)");
 constexpr int A_STAGE_BYTES = BM * KC;
 
 struct MmaShape {
@@ -113,7 +123,7 @@ struct MmaShape {
 };
 
 struct SmemPlan {
-    size_t steps, tables, bits, a, b, bars, total;
+    size_t steps, tables, bits, a, b, xch, bars, total;
 };
 
 // Tile buffer of 128 bit rows, kw words each, laid out [row / 32][word][row % 32]
@@ -141,6 +151,9 @@ __host__ __device__ inline SmemPlan smem_plan(const MmaShape& s) {
     o += (size_t)(s.gen ? 1 : s.nfy) * frr_table_len(s.n) * 2;
     if (s.gen) o = align_up(o + FRR_TABLE_SLACK, 16) + 16;
     o = align_up(o, 16);
+    p.xch = o;  // split epilogue: half sums handed between a quadrant's two tile warps
+    o += TW2 == 2 ? BM * sizeof(double) : 0;
+    o = align_up(o, 16);
     p.bars = o;
     o += 48 * 8 + 16;  // barriers + TMEM slot: also the FRR_TABLE_SLACK after the tables
     static_assert(48 * 8 + 16 >= FRR_TABLE_SLACK, "table slack");
@@ -154,7 +167,7 @@ __host__ __device__ inline void set_roles(MmaShape& s, int nfy, int nbits) {
     s.w_tma = nfy;
     s.w_mma = nfy + 1;
     s.w_tile0 = (nfy + 2 + 3) & ~3;
-    s.nwarps = s.w_tile0 + 4;
+    s.nwarps = s.w_tile0 + 4 * TW2;
 }
 
 __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.bars);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 46);
     // GEN 1: lock of the shared fixup table (last 16 bytes before the barriers)
-    int* fix_lock = reinterpret_cast<int*>(smem + P.bars - 16);
+    int* fix_lock = reinterpret_cast<int*>(smem + P.xch - 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (count + BM - 1) / BM;
@@ -253,7 +266,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (GEN) *fix_lock = 0;
         for (int b = 0; b < c_nbits; b++) {
             mbar_init(&bars[BAR_BITS_FULL + b], GEN ? 4 : c_nfy);
-            mbar_init(&bars[BAR_BITS_EMPTY + b], 4);
+            mbar_init(&bars[BAR_BITS_EMPTY + b], 4 * TW2);
         }
         for (int s = 0; s < S.nsta; s++) {
             mbar_init(&bars[BAR_A_FULL + s], 4);
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&bars[BAR_B_EMPTY + s], 1);
         }
         mbar_init(&bars[BAR_TMEM_FULL], 1);
-        mbar_init(&bars[BAR_TMEM_EMPTY], 4);
+        mbar_init(&bars[BAR_TMEM_EMPTY], 4 * TW2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -335,9 +348,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (lane == 0) mbar_arrive(&bars[BAR_BITS_FULL + buf]);
         }
-    } else if (warp >= c_w_tile0 && warp < c_w_tile0 + 4) {
+    } else if (warp >= c_w_tile0 && warp < c_w_tile0 + 4 * TW2) {
         // ============================================ expansion + epilogue
-        const int r = threadIdx.x - c_w_tile0 * 32;  // tile row == TMEM lane (warp % 4 = lane quadrant)
+        // quadrant warp `half` (of TW2) expands the K chunks kc % TW2 == half and,
+        // with TW2 = 2, evaluates columns 4 half .. 4 half + 3 of every 8-group
+        const int quad = (warp - c_w_tile0) & 3, half = (warp - c_w_tile0) >> 2;
+        const int r = quad * 32 + lane;  // tile row == TMEM lane (warp % 4 = lane quadrant)
         const double g = bal.g, cst = bal.cst;
         const int d = S.d, full = d - (d % 8);
         // |acc| <= 128 n would allow 32-bit limb pairs, but here (64-register
@@ -356,8 +372,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // row r: word w at [r / 32][w][r % 32]; control bits -> treated
             const uint32_t* row = sBits + (size_t)buf * buf_words + (size_t)(r >> 5) * S.kw * 32 + (r & 31);
             // A stages in TMEM: this warp's lane quadrant, columns after the accumulator
-            const uint32_t a_tl = tmem_base + ((uint32_t)((warp - c_w_tile0) * 32) << 16) + (uint32_t)S.npad;
+            const uint32_t a_tl = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)S.npad;
             for (int kc = 0; kc < S.nkc; kc++, astage++) {
+                if (TW2 == 2 && (kc & 1) != half) continue;
                 const int s = astage % S.nsta;
                 TW(2, mbar_wait(&bars[BAR_A_EMPTY + s], ((astage / S.nsta) & 1) ^ 1));
                 const uint32_t* src = row + (size_t)kc * (KC / 32) * 32;
@@ -401,13 +418,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
             TW(3, mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1));
             tc_fence_after();
-            const uint32_t tl = tmem_base + ((uint32_t)((warp - c_w_tile0) * 32) << 16);
+            const uint32_t tl = tmem_base + ((uint32_t)(quad * 32) << 16);
+            double res = -0.0;
+            if (TW2 == 2) {
+                // d <= 128: one leaf of numpy's pairwise sum.  This warp's 4 of the
+                // 8 accumulator streams, then ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7))
+                // across the pair of warps, then half 0 adds the tail in order.
+                double ra[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) ra[u] = 0.0;
+                for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : full); jb += 8) {
+                    int64_t Sj[4];
+                    tc_limbs4(tl + (uint32_t)(jb + 4 * half), S.L, S.dpad, true, Sj);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const double delta =
+                            __dsub_rn(__dmul_rn(__ll2double_rn(Sj[u]), g), bal.cc[jb + 4 * half + u]);
+                        const double q = __dmul_rn(delta, delta);
+                        ra[u] = jb == 0 ? q : __dadd_rn(ra[u], q);
+                    }
+                }
+                int64_t St[8];
+                if (half == 0 && full < d && !(FRR_MMA_DEBUG & 4)) tc_limbs8(tl + (uint32_t)full, S.L, S.dpad, true, St);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[BAR_TMEM_EMPTY]);
+                double* xch = reinterpret_cast<double*>(smem + P.xch);
+                const double part = __dadd_rn(__dadd_rn(ra[0], ra[1]), __dadd_rn(ra[2], ra[3]));
+                if (half == 1) xch[r] = part;
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+                if (half == 0) {
+                    res = __dadd_rn(part, xch[r]);
+                    if (!(FRR_MMA_DEBUG & 4))
+                        for (int u = 0; u < 8; u++)
+                            if (full + u < d) {
+                                const double delta =
+                                    __dsub_rn(__dmul_rn(__ll2double_rn(St[u]), g), bal.cc[full + u]);
+                                res = __dadd_rn(res, __dmul_rn(delta, delta));
+                            }
+                    const int64_t c = tile * BM + r;
+                    if (c < count) out[c] = __dmul_rn(__dadd_rn(0.0, res), cst);
+                }
+                // half 0 has read xch[r] before half 1 may rewrite it next tile
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+                continue;
+            }
             // d <= 128 here: one leaf of numpy's pairwise sum -- 8 accumulators
             // over the full groups, their tree, then the tail added in order
             double racc[8];
 #pragma unroll
             for (int k = 0; k < 8; k++) racc[k] = 0.0;
-            double res = -0.0;
             for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
                 if (jb >= d) break;
                 int64_t Sj[8];
@@ -500,7 +560,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 #if FRR_MMA_TIMING
     {
-        const int role = warp < c_nfy ? 8 : (warp >= c_w_tile0 && warp < c_w_tile0 + 4) ? 9 : (warp == c_w_mma ? 10 : 12);
+        const int role = warp < c_nfy ? 8 : (warp >= c_w_tile0 && warp < c_w_tile0 + 4 * TW2) ? 9 : (warp == c_w_mma ? 10 : 12);
         wacc[role] += clock64() - tstart;
         if (lane == 0)
             for (int k = 0; k < 16; k++)

@@ -229,47 +229,6 @@ __device__ __forceinline__ void mbar_wait_hw(uint64_t* b, uint32_t parity) {
 #endif
 }
 
-__device__ __forceinline__ void tc_ld4(uint32_t taddr, int32_t (&v)[4]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-                 : "r"(taddr)
-                 : "memory");
-}
-
-// exact S of 4 consecutive columns from L limbs (column l*stride + u), as tc_limbs8
-__device__ __forceinline__ void tc_limbs4(uint32_t base, int L, int stride, bool pair32, int64_t (&Sj)[4]) {
-    int l = L - 1;
-    if (pair32 && !(L & 1)) {
-#pragma unroll
-        for (int u = 0; u < 4; u++) Sj[u] = 0;
-    } else {
-        int32_t v[4];
-        tc_ld4(base + (uint32_t)(l * stride), v);
-        tc_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 4; u++) Sj[u] = v[u];
-        l--;
-    }
-    if (pair32) {
-        for (; l > 0; l -= 2) {
-            int32_t vh[4], vl[4];
-            tc_ld4(base + (uint32_t)(l * stride), vh);
-            tc_ld4(base + (uint32_t)((l - 1) * stride), vl);
-            tc_wait_ld();
-#pragma unroll
-            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 65536 + (int64_t)(vh[u] * 256 + vl[u]);
-        }
-    } else {
-        for (; l >= 0; l--) {
-            int32_t v[4];
-            tc_ld4(base + (uint32_t)(l * stride), v);
-            tc_wait_ld();
-#pragma unroll
-            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 256 + v[u];
-        }
-    }
-}
-
 __device__ __forceinline__ double comb8(const double (&r)[8]) {
     return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));

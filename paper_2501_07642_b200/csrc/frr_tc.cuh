@@ -199,6 +199,47 @@ __device__ __forceinline__ void tc_limbs8(uint32_t base, int L, int stride, bool
     }
 }
 
+__device__ __forceinline__ void tc_ld4(uint32_t taddr, int32_t (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// exact S of 4 consecutive columns from L limbs (column l*stride + u), as tc_limbs8
+__device__ __forceinline__ void tc_limbs4(uint32_t base, int L, int stride, bool pair32, int64_t (&Sj)[4]) {
+    int l = L - 1;
+    if (pair32 && !(L & 1)) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) Sj[u] = 0;
+    } else {
+        int32_t v[4];
+        tc_ld4(base + (uint32_t)(l * stride), v);
+        tc_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; u++) Sj[u] = v[u];
+        l--;
+    }
+    if (pair32) {
+        for (; l > 0; l -= 2) {
+            int32_t vh[4], vl[4];
+            tc_ld4(base + (uint32_t)(l * stride), vh);
+            tc_ld4(base + (uint32_t)((l - 1) * stride), vl);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 65536 + (int64_t)(vh[u] * 256 + vl[u]);
+        }
+    } else {
+        for (; l >= 0; l--) {
+            int32_t v[4];
+            tc_ld4(base + (uint32_t)(l * stride), v);
+            tc_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 4; u++) Sj[u] = Sj[u] * 256 + v[u];
+        }
+    }
+}
+
 // The same S_j from 32-bit limb pairs p_i = acc_{2i+1} * 256 + acc_{2i}
 // (|acc| <= 128 t, so |p| < 2^31 whenever t < 65280): one TMEM round trip
 // per pair, then S = sum_i p_i 2^(16 i) with two int64 multiply-adds for
