@@ -56,7 +56,10 @@ constexpr int A_STAGES = FRR_MMA_STAGES;
 #endif
 constexpr int A_TSTAGES = 8;  // max TMEM A stages
 constexpr int A_SLOTS = A_STAGES > A_TSTAGES ? A_STAGES : A_TSTAGES;
-constexpr int B_STAGES = FRR_MMA_STAGES;
+#ifndef FRR_MMA_BSTAGES
+#define FRR_MMA_BSTAGES FRR_MMA_STAGES
+#endif
+constexpr int B_STAGES = FRR_MMA_BSTAGES;
 constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: their tables share smem)
 // thread-per-candidate generators: RFY warps (4 per tile in flight, a
 // multiple of 4) building rows in place in RBITS tile buffers
@@ -97,6 +100,13 @@ __device__ unsigned long long g_frr_waits[16];
 // epilogue limb recombination through 32-bit limb pairs (tc_limbs8_pairs)
 #ifndef FRR_MMA_PAIRS
 #define FRR_MMA_PAIRS 1
+#endif
+// L = 6 epilogue: all limbs of 4 columns per TMEM round trip, software-pipelined
+#ifndef FRR_MMA_STAGGER
+#define FRR_MMA_STAGGER 0  // cycles: odd generator groups' start delay
+#endif
+#ifndef FRR_MMA_EPI_PIPE
+#define FRR_MMA_EPI_PIPE 0  // measured: no gain (the epilogue is not TMEM-latency bound)
 #endif
 // timing experiments only (results invalid): 1 no Fisher-Yates, 4 no epilogue,
 // 8 generators only (tile, copy and MMA roles just recycle the bit buffers)
@@ -296,6 +306,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // CTA's tiles g / 4, g / 4 + nfy / 4, ... in place in their buffers
         const int q = warp & 3, kstep = c_nfy >> 2;
         const uint32_t sst = smem_u32(ssteps);
+#if FRR_MMA_STAGGER
+        // desynchronise the tile groups' rounds: odd groups start half a job late
+        if ((warp >> 2) & 1) {
+            const long long t_end = clock64() + (long long)FRR_MMA_STAGGER;
+            while (clock64() < t_end) __nanosleep(1000);
+        }
+#endif
         for (int64_t k = warp >> 2;; k += kstep) {
             const int64_t tile = blockIdx.x + k * gridDim.x;
             if (tile >= ntiles) break;
@@ -417,6 +434,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
             // ---------------- epilogue: TMEM -> exact S -> fp64 statistic
             TW(3, mbar_wait_long(&bars[BAR_TMEM_FULL], i & 1));
+#if FRR_MMA_TIMING
+            const long long t_epi0 = clock64();
+#endif
             tc_fence_after();
             const uint32_t tl = tmem_base + ((uint32_t)(quad * 32) << 16);
             double res = -0.0;
@@ -468,7 +488,55 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             double racc[8];
 #pragma unroll
             for (int k = 0; k < 8; k++) racc[k] = 0.0;
-            for (int jb = 0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
+            int jb0 = 0;  // first group left for the generic loop below
+            if (FRR_MMA_EPI_PIPE && S.L == 6 && !(FRR_MMA_DEBUG & 4)) {
+                // L = 6 (the C2 shape): 4 columns x 6 limbs per TMEM round trip,
+                // the next 4 columns' loads in flight while this group's fp64
+                // work runs (the epilogue holds the single accumulator, so its
+                // latency is the consumer pipeline's critical path)
+                int32_t v[6][4];
+                int64_t Sc[4];
+                auto issue = [&](int j) {
+#pragma unroll
+                    for (int l = 0; l < 6; l++) tc_ld4(tl + (uint32_t)(l * S.dpad + j), v[l]);
+                };
+                auto combine = [&]() {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int32_t p0 = v[1][u] * 256 + v[0][u], p1 = v[3][u] * 256 + v[2][u],
+                                      p2 = v[5][u] * 256 + v[4][u];
+                        Sc[u] = ((int64_t)p2 * 65536 + p1) * 65536 + p0;
+                    }
+                };
+                auto accumulate = [&](int j, int s0, bool first) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const double delta = __dsub_rn(__dmul_rn(__ll2double_rn(Sc[u]), g), bal.cc[j + u]);
+                        const double q = __dmul_rn(delta, delta);
+                        racc[s0 + u] = first ? q : __dadd_rn(racc[s0 + u], q);
+                    }
+                };
+                if (full >= 8) {
+                    issue(0);
+                    tc_wait_ld();
+                    combine();
+                    for (int jb = 0; jb < full; jb += 8) {
+                        issue(jb + 4);
+                        accumulate(jb, 0, jb == 0);
+                        tc_wait_ld();
+                        combine();
+                        const bool more = jb + 8 < full;
+                        if (more) issue(jb + 8);
+                        accumulate(jb + 4, 4, jb == 0);
+                        if (more) {
+                            tc_wait_ld();
+                            combine();
+                        }
+                    }
+                    jb0 = full;
+                }
+            }
+            for (int jb = jb0; jb < ((FRR_MMA_DEBUG & 4) ? 0 : S.dpad); jb += 8) {
                 if (jb >= d) break;
                 int64_t Sj[8];
 #if FRR_MMA_PAIRS
@@ -499,6 +567,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars[BAR_TMEM_EMPTY]);
+#if FRR_MMA_TIMING
+            wacc[13] += clock64() - t_epi0;  // epilogue: TMEM full -> drained
+#endif
             if (d >= 8 && full == d)
                 res = __dadd_rn(__dadd_rn(__dadd_rn(racc[0], racc[1]), __dadd_rn(racc[2], racc[3])),
                                 __dadd_rn(__dadd_rn(racc[4], racc[5]), __dadd_rn(racc[6], racc[7])));

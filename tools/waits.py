@@ -27,8 +27,9 @@ G.mc_stats_device(kern, design, 0, M, out)
 N.lib().frr_debug_waits(buf)
 w = list(buf)
 names = ["FY bits_empty", "tile bits_full", "tile a_empty", "tile tmem_full", "TMA b_empty", "MMA tmem_empty",
-         "MMA a_full", "MMA b_full", "FY total", "tile total", "MMA total", "FY in warp_fy"]
-tot = {0: 8, 11: 8, 1: 9, 2: 9, 3: 9, 5: 10, 6: 10, 7: 10}
+         "MMA a_full", "MMA b_full", "FY total", "tile total", "MMA total", "FY in warp_fy", "TMA total",
+         "tile epilogue"]
+tot = {0: 8, 11: 8, 1: 9, 2: 9, 3: 9, 13: 9, 5: 10, 6: 10, 7: 10}
 for k, nm in enumerate(names):
     frac = f"{100 * w[k] / w[tot[k]]:6.2f}% of role" if k in tot and w[tot[k]] else ""
     print(f"{nm:16s} {w[k]:>18d} {frac}")
