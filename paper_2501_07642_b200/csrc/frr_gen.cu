@@ -904,24 +904,107 @@ __device__ __forceinline__ void dim_terms(double v, uint32_t treated_bit, double
     vc = __dmul_rn(nw, v);
 }
 
-// b, membership and the pairwise sums of one lane's key: word(w) = the
-// key's control bits of units 32 w .. 32 w + 31; the sums are left on the
-// lane's stack (stk[0] = treated, stk[32] = control); y may be shared or global.
-template <class Word>
-__device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict__ y, const uint32_t* __restrict__ obs,
-                                     Word col_word, const int* leaf_off, const int* leaf_len, const int16_t* tok,
-                                     int ntok, double* stk, uint32_t& pt_out, uint32_t& pc_out, bool& same_out) {
-    // b and membership (exact integer popcounts)
+// FRR_DIM_FMA (default): r += w*y as one fused multiply-add.  For w in
+// {0, 1} the product w*y is exact, so fma(w, y, r) -- one rounding of
+// w*y + r, zero signs by the rules of addition -- is bit-identical to
+// numpy's separately rounded (w*y) then r + (w*y), and numpy's first term
+// r_j = w*y equals fma(w, y, -0.0).  Two DFMAs per unit instead of two
+// DMULs and two DADDs.
+#ifndef FRR_DIM_FMA
+#define FRR_DIM_FMA 1
+#endif
+
+// ctl != 0: the unit is a control unit of this key (w = 0)
+__device__ __forceinline__ void dim_acc(double& st, double& sc, double v, uint32_t ctl) {
+    const int wh = ctl ? 0 : 0x3FF00000;
+    st = __fma_rn(__hiloint2double(wh, 0), v, st);
+    sc = __fma_rn(__hiloint2double(wh ^ 0x3FF00000, 0), v, sc);
+}
+
+// b and membership of one bitset word (exact integer popcounts)
+struct DimCounts {
     uint32_t pt = 0, pc = 0;
     bool same = true;
-    for (int w = 0; w < kw; w++) {
+    __device__ __forceinline__ void add(uint32_t ctl_word, int w, int n, const uint32_t* __restrict__ obs) {
         const int valid = n - 32 * w;
         const uint32_t vm = valid >= 32 ? FRR_FULL : ((1u << valid) - 1u);
-        const uint32_t tr = ~col_word(w) & vm, o = __ldg(obs + w);
+        const uint32_t tr = ~ctl_word & vm, o = __ldg(obs + w);
         pt += __popc(tr & o);
         pc += __popc(~tr & vm & o);
         same &= tr == o;
     }
+};
+
+// a lane's control words in shared memory (word w at col[32 w])
+struct DimWordsShared {
+    static constexpr bool kStream = false;
+    const uint32_t* col;
+    __device__ __forceinline__ uint32_t operator()(int w) const { return col[32 * w]; }
+};
+
+// a lane's control words in global memory, read once each in ascending
+// order (the pairwise walk visits units left to right): kDimRing words in
+// flight through a per-lane ring in shared memory (cp.async, one commit
+// group per word, so a word's wait never waits on a register move of a
+// load still in flight); each word's popcounts are taken as it retires
+constexpr int kDimRing = 8;
+
+struct DimWordsRing {
+    static constexpr bool kStream = true;
+    const uint32_t* col;  // word w at col[32 w]
+    uint32_t ring;        // shared address of this lane's slot 0 (slot s at ring + 128 s)
+    int kw, n, cw;
+    const uint32_t* obs;
+    uint32_t cur;
+    DimCounts cnt;
+    __device__ __forceinline__ void fetch(int w) {
+        if (w < kw)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ring + 128u * (uint32_t)(w % kDimRing)),
+                         "l"(col + 32 * (size_t)w)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __device__ __forceinline__ uint32_t slot(int w) const {
+        uint32_t v;
+        asm volatile("cp.async.wait_group %1;\n\tld.shared.u32 %0, [%2];"
+                     : "=r"(v)
+                     : "n"(kDimRing - 1), "r"(ring + 128u * (uint32_t)(w % kDimRing))
+                     : "memory");
+        return v;
+    }
+    __device__ __forceinline__ DimWordsRing(const uint32_t* c, uint32_t r, int kw_, int n_, const uint32_t* o)
+        : col(c), ring(r), kw(kw_), n(n_), cw(0), obs(o) {
+#pragma unroll
+        for (int d = 0; d < kDimRing; d++) fetch(d);
+        cur = slot(0);
+    }
+    __device__ __forceinline__ void advance() {
+        cnt.add(cur, cw, n, obs);
+        fetch(cw + kDimRing);  // into the slot of word cw, already in `cur`
+        cw++;
+        cur = slot(cw);
+    }
+    __device__ __forceinline__ uint32_t operator()(int w) {
+        if (w != cw) advance();  // w == cw or cw + 1
+        return cur;
+    }
+    __device__ __forceinline__ void finish() {
+        while (cw < kw - 1) advance();
+        cnt.add(cur, cw, n, obs);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+};
+
+// b, membership and the pairwise sums of one lane's key: words(w) = the
+// key's control bits of units 32 w .. 32 w + 31; the sums are left on the
+// lane's stack (stk[0] = treated, stk[32] = control); y may be shared or global.
+template <class Words>
+__device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict__ y, const uint32_t* __restrict__ obs,
+                                         Words& col_word, const int* leaf_off, const int* leaf_len, const int16_t* tok,
+                                         int ntok, double* stk, uint32_t& pt_out, uint32_t& pc_out, bool& same_out) {
+    DimCounts cnt;
+    if constexpr (!Words::kStream)
+        for (int w = 0; w < kw; w++) cnt.add(col_word(w), w, n, obs);
     // ---- a: numpy's pairwise sums of w*y and (1-w)*y, token program
     int sp = 0;
     for (int k = 0; k < ntok; k++) {
@@ -934,6 +1017,41 @@ __device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict
         }
         const int off = leaf_off[L], len = leaf_len[L];
         double st, sc;
+#if FRR_DIM_FMA
+        if (len < 8) {
+            st = sc = -0.0;
+            for (int i = 0; i < len; i++) {
+                const int e = off + i;
+                dim_acc(st, sc, y[e], (col_word(e >> 5) >> (e & 31)) & 1u);
+            }
+        } else {
+            // 8 accumulators: r_j = term[j] + term[j + 8] + ... (off is a
+            // multiple of 8, so units e..e+7 share one bitset word)
+            const int full = len - (len % 8);
+            double rt[8], rc[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) rt[j] = rc[j] = -0.0;
+            for (int i = 0; i < full; i += 8) {
+                const int e = off + i;
+                const uint32_t bits = col_word(e >> 5) >> (e & 31);
+                const double2* yv = reinterpret_cast<const double2*>(y + e);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const double2 v2 = yv[q];
+                    dim_acc(rt[2 * q], rc[2 * q], v2.x, bits & (1u << (2 * q)));
+                    dim_acc(rt[2 * q + 1], rc[2 * q + 1], v2.y, bits & (2u << (2 * q)));
+                }
+            }
+            st = __dadd_rn(__dadd_rn(__dadd_rn(rt[0], rt[1]), __dadd_rn(rt[2], rt[3])),
+                           __dadd_rn(__dadd_rn(rt[4], rt[5]), __dadd_rn(rt[6], rt[7])));
+            sc = __dadd_rn(__dadd_rn(__dadd_rn(rc[0], rc[1]), __dadd_rn(rc[2], rc[3])),
+                           __dadd_rn(__dadd_rn(rc[4], rc[5]), __dadd_rn(rc[6], rc[7])));
+            for (int i = full; i < len; i++) {  // the tail, in order
+                const int e = off + i;
+                dim_acc(st, sc, y[e], (col_word(e >> 5) >> (e & 31)) & 1u);
+            }
+        }
+#else
         if (len < 8) {
             st = sc = -0.0;
             for (int i = 0; i < len; i++) {
@@ -944,8 +1062,6 @@ __device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict
                 sc = __dadd_rn(sc, vc);
             }
         } else {
-            // 8 accumulators: r_j = term[j] + term[j + 8] + ... (off is a
-            // multiple of 8, so units e..e+7 share one bitset word)
             const int full = len - (len % 8);
             double rt[8], rc[8];
             {
@@ -978,7 +1094,7 @@ __device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict
                            __dadd_rn(__dadd_rn(rt[4], rt[5]), __dadd_rn(rt[6], rt[7])));
             sc = __dadd_rn(__dadd_rn(__dadd_rn(rc[0], rc[1]), __dadd_rn(rc[2], rc[3])),
                            __dadd_rn(__dadd_rn(rc[4], rc[5]), __dadd_rn(rc[6], rc[7])));
-            for (int i = full; i < len; i++) {  // the tail, in order
+            for (int i = full; i < len; i++) {
                 const int e = off + i;
                 double vt, vc;
                 dim_terms(y[e], ~(col_word(e >> 5) >> (e & 31)) & 1u, vt, vc);
@@ -986,13 +1102,18 @@ __device__ __forceinline__ void dim_lane(int n, int kw, const double* __restrict
                 sc = __dadd_rn(sc, vc);
             }
         }
+#endif
         stk[(2 * sp) * 32] = st;
         stk[(2 * sp + 1) * 32] = sc;
         sp++;
     }
-    pt_out = pt;
-    pc_out = pc;
-    same_out = same;
+    if constexpr (Words::kStream) {
+        col_word.finish();
+        cnt = col_word.cnt;
+    }
+    pt_out = cnt.pt;
+    pc_out = cnt.pc;
+    same_out = cnt.same;
 }
 
 __global__ void __launch_bounds__(kDimRevWarps * 32) k_dim_rev(uint64_t seed, const uint64_t* __restrict__ ids,
@@ -1043,7 +1164,8 @@ __global__ void __launch_bounds__(kDimRevWarps * 32) k_dim_rev(uint64_t seed, co
         __syncwarp();
         uint32_t pt, pc;
         bool same;
-        dim_lane(n, kw, y, obs, [&](int w) { return col[32 * w]; }, leaf_off, leaf_len, tok, ntok, stk, pt, pc, same);
+        DimWordsShared cw{col};
+        dim_lane(n, kw, y, obs, cw, leaf_off, leaf_len, tok, ntok, stk, pt, pc, same);
         if (c < m) {
             const double s_t = __dadd_rn(0.0, stk[0]), s_c = __dadd_rn(0.0, stk[32]);
             a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
@@ -1062,7 +1184,7 @@ constexpr int kDimBitsWarps = 8;
 
 struct DimBitsPlan {
     int kw, maxl;
-    size_t y_off, plan_off, stk_off, total;
+    size_t y_off, plan_off, stk_off, ring_off, total;
 };
 
 DimBitsPlan dim_bits_plan(int n) {
@@ -1078,6 +1200,8 @@ DimBitsPlan dim_bits_plan(int n) {
     o = (o + 15) & ~(size_t)15;
     p.stk_off = o;
     o += (size_t)kDimBitsWarps * kDimStack * 2 * 32 * sizeof(double);
+    p.ring_off = o;
+    o += (size_t)kDimBitsWarps * kDimRing * 32 * sizeof(uint32_t);
     p.total = o;
     return p;
 }
@@ -1103,6 +1227,7 @@ __global__ void __launch_bounds__(kDimBitsWarps * 32) k_dim_bits(const uint32_t*
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kw = P.kw;
     double* stk = reinterpret_cast<double*>(smem + P.stk_off) + (size_t)warp * kDimStack * 2 * 32 + lane;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem + P.ring_off) + 4u * (uint32_t)(warp * kDimRing * 32 + lane);
     const double inv_t = 1.0 / (double)t, inv_c = 1.0 / (double)(n - t);
     const int64_t njobs = (m + 31) / 32;
     for (int64_t job = (int64_t)blockIdx.x * kDimBitsWarps + warp; job < njobs;
@@ -1111,8 +1236,8 @@ __global__ void __launch_bounds__(kDimBitsWarps * 32) k_dim_bits(const uint32_t*
         const uint32_t* col = words + (size_t)job * kw * 32 + lane;  // coalesced: one 128-byte row per word
         uint32_t pt, pc;
         bool same;
-        dim_lane(n, kw, sy, obs, [&](int w) { return __ldg(col + 32 * w); }, leaf_off, leaf_len, tok, ntok, stk, pt,
-                 pc, same);
+        DimWordsRing cw(col, ring, kw, n, obs);
+        dim_lane(n, kw, sy, obs, cw, leaf_off, leaf_len, tok, ntok, stk, pt, pc, same);
         if (c < m) {
             const double s_t = __dadd_rn(0.0, stk[0]), s_c = __dadd_rn(0.0, stk[32]);
             a[c] = __dsub_rn(__dmul_rn(s_t, inv_t), __dmul_rn(s_c, inv_c));
@@ -1474,6 +1599,7 @@ extern "C" int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, 
 
 int frr_rev_words(uint64_t root_seed, const uint64_t* ids, int64_t count, int n, int t, uint32_t* words,
                   void* steps, void* stream);
+int64_t frr_rev_wave_keys(int n, int t);
 
 // workspace of frr_dim_mc_ws: the generator's global step table (64 KB per
 // 4096 steps, t <= FRR_MAX_UNITS) then the bitsets of a chunk of keys (a
@@ -1498,7 +1624,12 @@ extern "C" int frr_dim_mc_ws(uint64_t root_seed, const uint64_t* draws, int64_t 
     int rc = check_nt(n, t);
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
-    const int64_t chunk = dim_ws_chunk(n, ws_bytes);
+    int64_t chunk = dim_ws_chunk(n, ws_bytes);
+    // whole generator waves per chunk: a chunk of 2^18 keys at n = 5000 is
+    // 5.03 waves of 11 warps x 148 SMs, i.e. 6 rounds of which the last is
+    // almost idle
+    const int64_t wave = frr_rev_wave_keys(n, t);
+    if (wave > 0 && chunk >= wave && m > chunk) chunk = chunk / wave * wave;
     const DimBitsPlan P = dim_bits_plan(n);
     if (chunk < 32 || P.total > 227 * 1024)
         return frr_dim_mc(root_seed, draws, m, n, t, y, obs_bits, a, b, match, stream);

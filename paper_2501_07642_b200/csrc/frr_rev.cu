@@ -10,6 +10,10 @@
 #include "frr_launch.cuh"
 #include "frr_revfy.cuh"
 
+#ifndef FRR_REV_BATCH
+#define FRR_REV_BATCH 0  // 1: batched bit moves per group (frr_rev_move_group; bit-exact, measured 7% slower at n = 5000)
+#endif
+
 namespace {
 constexpr int kRevWarps = 16;
 
@@ -71,7 +75,7 @@ __global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, cons
         const int64_t c = job * 32 + lane;
         const uint64_t state =
             frr_derive_state(seed, ids ? ids[c < count ? c : count - 1] : lo + (uint64_t)c);
-        const bool flag = frr_rev_fy<GS>(state, t, sst, wsa, P.kw);
+        const bool flag = frr_rev_fy<GS, FRR_REV_BATCH>(state, t, sst, wsa, P.kw);
         uint32_t fl = __ballot_sync(FRR_FULL, flag);
         while (fl) {
             const int src = __ffs(fl) - 1;
@@ -101,6 +105,22 @@ __global__ void k_fill_steps_ws(StepC* steps, int n, int t) {
         steps[k] = frr_make_step(k < t ? n : k + 1, k);
 }
 
+// the global step table (when the caller provides one) unless the shared
+// copy leaves as many warps' bitsets room (n = 5000: 11 warps instead of 9,
+// +7% through frr_dim_mc_ws)
+static bool rev_use_gsteps(int n, int t) { return rev_plan(n, t, false).warps < rev_plan(n, t, true).warps; }
+
+// keys per full wave of the generator (every resident warp busy once) when
+// the caller provides a global step table; 0 on error
+int64_t frr_rev_wave_keys(int n, int t) {
+    if (n < 2 || t < 1 || t >= n || n > FRR_MAX_UNITS) return 0;
+    const bool gs = rev_use_gsteps(n, t);
+    const RevPlan P = rev_plan(n, t, gs);
+    const auto kern = gs ? k_rev_bits<true> : k_rev_bits<false>;
+    if (P.total > 227 * 1024 || frr_prepare_kernel(kern, P.total)) return 0;
+    return (int64_t)frr_persistent_grid(kern, P.warps * 32, P.total, INT64_MAX) * P.warps * 32;
+}
+
 // gsteps: caller memory of frr_steps_len(t) * 16 bytes for a global step
 // table (NULL: shared copy per CTA)
 static int rev_launch(uint64_t root_seed, const uint64_t* ids, uint64_t draw_lo, int64_t count, int n, int t,
@@ -110,9 +130,7 @@ static int rev_launch(uint64_t root_seed, const uint64_t* ids, uint64_t draw_lo,
         return FRR_E_INVALID_DESIGN;
     }
     if (count <= 0) return FRR_OK;
-    // the shared step table wins while it leaves 6 or more warps (measured at
-    // n = 5000: 8 warps with shared steps beat 11 with global ones by 9%)
-    if (gsteps && rev_plan(n, t, false).warps >= 6) gsteps = nullptr;
+    if (gsteps && !rev_use_gsteps(n, t)) gsteps = nullptr;
     const RevPlan P = rev_plan(n, t, gsteps != nullptr);
     if (P.total > 227 * 1024) {
         frr_set_error("frr_rev_bits: n=%d too large for the shared bitsets", n);
