@@ -223,8 +223,12 @@ int frr_dim_mc(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int 
  * shared memory, chunk by chunk (the workspace holds ws_bytes / (4 ceil(n/32))
  * keys, a multiple of 32).  Same results as frr_dim_mc; falls back to it when
  * the workspace holds fewer than 32 keys.  frr_dim_mc_workspace_bytes: the
- * size that serves m keys in chunks of up to 2^18. */
+ * size that serves m keys in chunks of up to 2^18.  frr_dim_mc_chunk_keys:
+ * the keys per internal chunk for m keys and that workspace size (whole
+ * generator waves) -- the granularity at which a caller streaming keys in
+ * can split the call without changing the launch shapes. */
 size_t frr_dim_mc_workspace_bytes(int64_t m, int n);
+int64_t frr_dim_mc_chunk_keys(int64_t m, int n, int t, size_t ws_bytes);
 int frr_dim_mc_ws(uint64_t root_seed, const uint64_t* draws, int64_t m, int n, int t,
                   const double* y, const uint32_t* obs_bits, double* a, double* b, int32_t* match,
                   void* workspace, size_t ws_bytes, void* stream);

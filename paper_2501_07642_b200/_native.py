@@ -78,6 +78,7 @@ SIGNATURES = {
     "frr_sort_pairs": (i32, [vp, vp, i64, i32, vp, sz, vp]),
     "frr_dim_mc": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_mc_workspace_bytes": (sz, [i64, i32]),
+    "frr_dim_mc_chunk_keys": (i64, [i64, i32, i32, sz]),
     "frr_dim_mc_ws": (i32, [u64, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
     "frr_dim_exact": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "frr_dim_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
@@ -179,31 +180,133 @@ def _stage_ring():
 
 
 def to_host(t):
-    """Device tensor -> numpy array (a fresh, caller-owned array); see to_host_many."""
+    """Device tensor -> a numpy array the caller owns; see to_host_many."""
     return to_host_many(t)[0]
 
 
+# Recycled page-locked result buffers.  A large result is copied by one DMA
+# straight into a page-locked slab that the caller's numpy array views; when
+# the last view of that array dies, the slab returns to the pool for the next
+# result (PEP 688 buffer release), so repeated calls neither page-lock nor
+# first-touch (~10 GB/s of page faults) new memory.  The pool is bounded:
+# FRR_HOST_POOL_MB (default 1024; 0 disables) of page-locked memory at most,
+# beyond which results go through the staging ring below.
+HOST_POOL_BYTES = int(os.environ.get("FRR_HOST_POOL_MB", "1024")) << 20
+HOST_POOL_ALIGN = 2 << 20
+_pool_lock = threading.Lock()
+_pool = {"free": [], "bytes": 0}
+
+
+class _PooledResult:
+    """Buffer exporter of one result: a byte range of a pooled slab."""
+
+    __slots__ = ("slab", "nbytes")
+
+    def __init__(self, slab, nbytes):
+        self.slab = slab
+        self.nbytes = nbytes
+
+    def __buffer__(self, flags):
+        return memoryview(self.slab.numpy()[: self.nbytes])
+
+    def __release_buffer__(self, view):
+        view.release()
+        slab, self.slab = self.slab, None
+        if slab is not None:
+            with _pool_lock:
+                _pool["free"].append(slab)
+
+
+def _pool_take(nbytes):
+    """A free slab of at least nbytes (best fit within 2x), a new one while
+    the pool is under its bound, or None."""
+    torch = torch_mod()
+    with _pool_lock:
+        free = _pool["free"]
+        fits = [i for i, s in enumerate(free) if nbytes <= s.numel() <= 2 * nbytes + HOST_POOL_ALIGN]
+        if fits:
+            i = min(fits, key=lambda i: free[i].numel())
+            return free.pop(i)
+        size = -(-nbytes // HOST_POOL_ALIGN) * HOST_POOL_ALIGN
+        if _pool["bytes"] + size > HOST_POOL_BYTES:
+            return None
+        _pool["bytes"] += size
+    return torch.empty(size, dtype=torch.uint8, pin_memory=True)
+
+
+def _np_dtype(t):
+    torch = torch_mod()
+    return torch.empty(0, dtype=t.dtype).numpy().dtype
+
+
 def to_host_many(*tensors):
-    """Device tensors -> fresh, caller-owned numpy arrays.  Large results
-    (accepted indices, statistics, assignment rows) stream through a fixed
-    ring of page-locked staging slots, all tensors in one pipeline: the DMA
-    of chunk i + 1 overlaps the host copy of chunk i out of its slot, and a
-    slot is reused once its host copy has finished (a pageable .cpu() of the
-    79 MB C4 row matrix runs at ~2 GB/s).  No page-locked memory is handed to
-    callers and the staging footprint does not grow with the result."""
+    """Device tensors -> numpy arrays the caller owns.  Large results
+    (accepted indices, statistics, assignment rows) are DMA'd into recycled
+    page-locked slabs (above) that the returned arrays view, all on one
+    stream with one synchronisation.  Results that do not fit the pool's
+    bound stream through a fixed ring of page-locked staging slots into fresh
+    numpy arrays: the DMA of chunk i + 1 overlaps the host copy of chunk i out
+    of its slot (a pageable .cpu() of the 79 MB C4 row matrix runs at
+    ~2 GB/s)."""
     torch = torch_mod()
     import numpy as np
 
     outs = [None] * len(tensors)
     big = []
+    dma = None
     for i, t in enumerate(tensors):
         nbytes = t.numel() * t.element_size()
         if not t.is_cuda or nbytes < STAGE_MIN_BYTES:
             outs[i] = t.cpu().numpy()
-        else:
+            continue
+        slab = _pool_take(nbytes)
+        if slab is None:
             big.append(i)
+            continue
+        t = t.contiguous()
+        slab[:nbytes].copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+        outs[i] = np.frombuffer(_PooledResult(slab, nbytes), dtype=_np_dtype(t)).reshape(tuple(t.shape))
+        dma = torch.cuda.current_stream(t.device)
+    if dma is not None:
+        dma.synchronize()
     if not big:
         return outs
+    from concurrent.futures import ThreadPoolExecutor
+
+    with _stage_lock:
+        ring = _stage_ring()
+        if _stage["pool"] is None:
+            # host copies of different slots run in parallel (np.copyto drops the GIL)
+            _stage["pool"] = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)))
+        pending = [None] * STAGE_SLOTS  # host-copy future per slot
+
+        def land(slot, dst, a, n, ev):
+            ev.synchronize()
+            np.copyto(dst[a:a + n], ring[slot].numpy()[:n])
+
+        k = 0
+        for i in big:
+            t = tensors[i].contiguous()
+            out = np.empty(tuple(t.shape), dtype=_np_dtype(t))
+            outs[i] = out
+            dst = out.reshape(-1).view(np.uint8)
+            flat = t.reshape(-1).view(torch.uint8)
+            nbytes = flat.numel()
+            stream = torch.cuda.current_stream(t.device)
+            for a in range(0, nbytes, STAGE_CHUNK):
+                slot = k % STAGE_SLOTS
+                k += 1
+                if pending[slot] is not None:
+                    pending[slot].result()  # the slot's previous chunk has left it
+                n = min(STAGE_CHUNK, nbytes - a)
+                ring[slot][:n].copy_(flat[a:a + n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                pending[slot] = _stage["pool"].submit(land, slot, dst, a, n, ev)
+        for f in pending:
+            if f is not None:
+                f.result()
+    return outs
     from concurrent.futures import ThreadPoolExecutor
 
     with _stage_lock:

@@ -1612,6 +1612,22 @@ static int64_t dim_ws_chunk(int n, size_t ws_bytes) {
     return (int64_t)((ws_bytes - dim_ws_steps_bytes()) / per_key) / 32 * 32;
 }
 
+// keys per internal chunk: whole generator waves (a chunk of 2^18 keys at
+// n = 5000 is 5.03 waves of 11 warps x 148 SMs, i.e. 6 rounds of which the
+// last is almost idle)
+static int64_t dim_ws_chunk_aligned(int64_t m, int n, int t, size_t ws_bytes) {
+    int64_t chunk = dim_ws_chunk(n, ws_bytes);
+    const int64_t wave = frr_rev_wave_keys(n, t);
+    if (wave > 0 && chunk >= wave && m > chunk) chunk = chunk / wave * wave;
+    return chunk;
+}
+
+extern "C" int64_t frr_dim_mc_chunk_keys(int64_t m, int n, int t, size_t ws_bytes) {
+    if (m <= 0 || n < 2 || t < 1 || t >= n) return 0;
+    const int64_t chunk = dim_ws_chunk_aligned(m, n, t, ws_bytes);
+    return chunk < 32 ? m : std::min(chunk, m);
+}
+
 extern "C" size_t frr_dim_mc_workspace_bytes(int64_t m, int n) {
     if (m <= 0 || n < 2) return 0;
     const int64_t keys = std::min<int64_t>((m + 31) / 32 * 32, (int64_t)1 << 18);
@@ -1624,12 +1640,7 @@ extern "C" int frr_dim_mc_ws(uint64_t root_seed, const uint64_t* draws, int64_t 
     int rc = check_nt(n, t);
     if (rc) return rc;
     if (m <= 0) return FRR_OK;
-    int64_t chunk = dim_ws_chunk(n, ws_bytes);
-    // whole generator waves per chunk: a chunk of 2^18 keys at n = 5000 is
-    // 5.03 waves of 11 warps x 148 SMs, i.e. 6 rounds of which the last is
-    // almost idle
-    const int64_t wave = frr_rev_wave_keys(n, t);
-    if (wave > 0 && chunk >= wave && m > chunk) chunk = chunk / wave * wave;
+    const int64_t chunk = dim_ws_chunk_aligned(m, n, t, ws_bytes);
     const DimBitsPlan P = dim_bits_plan(n);
     if (chunk < 32 || P.total > 227 * 1024)
         return frr_dim_mc(root_seed, draws, m, n, t, y, obs_bits, a, b, match, stream);

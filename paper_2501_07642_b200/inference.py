@@ -125,13 +125,9 @@ class _PoolStats:
                 # raises this for a pool without keys (generation.py:349-352)
                 raise InvalidDesignError(
                     "pool stores no keys; exact-mode pools carry explicit assignments instead")
-            draws = keymod.to_device_u64(np.ascontiguousarray(pool.keys[lo:hi, 1], dtype=np.uint64))
             if hi > lo:
-                ws_bytes = int(N.lib().frr_dim_mc_workspace_bytes(hi - lo, n))
-                ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=dev)
-                N.call("frr_dim_mc_ws", int(d.root_seed) & keymod.MASK64, N.ptr(draws), hi - lo, n, t,
-                       N.ptr(y_dev), N.ptr(obs_dev), N.ptr(a), N.ptr(b), N.ptr(match), N.ptr(ws), ws_bytes,
-                       N.stream_ptr())
+                self._dim_keys(pool.keys[lo:hi], int(d.root_seed) & keymod.MASK64, n, t, y_dev, obs_dev, a, b,
+                               match)
         if comm.world > 1:
             comm.all_reduce_(match)
         self.a_local, self.b_local = a, b
@@ -145,6 +141,40 @@ class _PoolStats:
                N.ptr(ab[1:2]), None, N.stream_ptr())
         tau_obs, b_obs = ab.cpu().tolist()
         self.tau_obs, self.b_obs = float(tau_obs), float(b_obs)
+
+    @staticmethod
+    def _dim_keys(keys, root_seed, n, t, y_dev, obs_dev, a, b, match):
+        """frr_dim_mc_ws over the keys [m, 2] (host), chunk by chunk: the
+        upload of chunk i + 1 runs on a side stream under the statistics of
+        chunk i (the library's own chunks, so launch shapes do not change)."""
+        torch = N.torch_mod()
+        dev = a.device
+        m = int(keys.shape[0])
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)
+        ws_bytes = int(N.lib().frr_dim_mc_workspace_bytes(m, n))
+        ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=dev)
+        chunk = max(1, int(N.lib().frr_dim_mc_chunk_keys(m, n, t, ws_bytes)))
+        main = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(main)
+
+        def upload(lo):
+            with torch.cuda.stream(side):
+                kd = torch.from_numpy(keys[lo:lo + chunk]).to(dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            return kd, ev
+
+        nxt = upload(0)
+        for lo in range(0, m, chunk):
+            kd, ev = nxt
+            main.wait_event(ev)
+            kd.record_stream(main)
+            draws = kd[:, 1].contiguous()
+            N.call("frr_dim_mc_ws", root_seed, N.ptr(draws), int(kd.shape[0]), n, t, N.ptr(y_dev), N.ptr(obs_dev),
+                   N.ptr(a[lo:]), N.ptr(b[lo:]), N.ptr(match), N.ptr(ws), ws_bytes, N.stream_ptr())
+            if lo + chunk < m:
+                nxt = upload(lo + chunk)  # (a pageable upload blocks the host while chunk lo computes)
 
     @property
     def a(self):

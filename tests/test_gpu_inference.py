@@ -99,6 +99,39 @@ def test_large_keys_pool_vs_oracle():
     assert got.tolist() == want
 
 
+def test_chunked_key_stream_equals_single_kernel():
+    """A keys pool larger than one workspace chunk (3e5 keys at n=5000): the
+    pipelined chunk-by-chunk upload + frr_dim_mc_ws equals the single-kernel
+    frr_dim_mc on every key, and a sample across the chunk boundaries equals
+    the C oracle."""
+    import torch
+
+    from paper_2501_07642_b200 import _native as N
+    from paper_2501_07642_b200.inference import _PoolStats
+
+    m = 300_000
+    pool = _t5k_pool(m)
+    chunk = int(N.lib().frr_dim_mc_chunk_keys(m, 5000, 2500, N.lib().frr_dim_mc_workspace_bytes(m, 5000)))
+    assert 32 <= chunk < m
+    W0 = frr.batch_assignments(5, np.array([0], dtype=np.uint64), 5000, 2500)[0]
+    y = np.random.default_rng(57).standard_normal(5000) + W0
+    ps = _PoolStats(pool, W0, y)
+    dev = N.device()
+    draws = torch.from_numpy(pool.keys[:, 1].astype(np.int64)).to(dev)
+    y_dev = torch.from_numpy(y).to(dev)
+    from paper_2501_07642_b200.inference import _pack_bits
+
+    obs = torch.from_numpy(_pack_bits(W0).view(np.int32)).to(dev)
+    a = torch.empty(m, dtype=torch.float64, device=dev)
+    b = torch.empty(m, dtype=torch.float64, device=dev)
+    N.call("frr_dim_mc", 5, N.ptr(draws), m, 5000, 2500, N.ptr(y_dev), N.ptr(obs), N.ptr(a), N.ptr(b), None,
+           N.stream_ptr())
+    assert torch.equal(ps.a_local, a) and torch.equal(ps.b_local, b)
+    pick = np.unique(np.concatenate([np.arange(chunk - 40, chunk + 40), np.arange(m - 40, m), np.arange(40)]))
+    W = O.c_batch_assign(5, (997 * pick).astype(np.uint64), 5000, 2500)
+    assert np.array_equal(ps.a_local.cpu().numpy()[pick], O.c_dim_rows(W, y, 2500))
+
+
 def test_keys_pool_t_near_n_vs_oracle():
     """k_dim with t = n - 1, n a multiple of 32 (padding steps re-read past the table)."""
     n, t, m = 1056, 1055, 3000

@@ -167,7 +167,7 @@ def c5(m=10**6):
     def stats():
         ps[0] = _PoolStats(pool, obs, y)
 
-    s_keys = timed(stats, reps=2)
+    s_keys = timed(stats, reps=5)
     p = ps[0]
     sd = float(np.std(p.a.cpu().numpy()))
     taus = np.linspace(p.tau_obs - 10 * sd, p.tau_obs + 10 * sd, 512)
