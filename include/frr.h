@@ -278,6 +278,9 @@ int frr_microbench_draws(int64_t per_thread, uint64_t* sink, int64_t* total_draw
  * bit 1 set: random operand bytes instead of zeros.
  * *ops_host = 2*M*N*K*instructions (int8 ops) of the launch. */
 int frr_microbench_mma_i8(int N, int a_tmem, int64_t iters, int64_t* ops_host, void* stream);
+/* The same for CTA pairs (clusters of 2, tcgen05.mma.cta_group::2, M=256,
+ * B split by N between the two CTAs); N a multiple of 32. */
+int frr_microbench_mma_i8_pair(int N, int a_tmem, int64_t iters, int64_t* ops_host, void* stream);
 
 #ifdef __cplusplus
 }

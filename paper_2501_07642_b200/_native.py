@@ -86,6 +86,7 @@ SIGNATURES = {
     "frr_selftest_mma_i8": (i32, [vp, vp, i32, i32, vp, i32, vp]),
     "frr_microbench_draws": (i32, [i64, vp, vp, vp]),
     "frr_microbench_mma_i8": (i32, [i32, i32, i64, vp, vp]),
+    "frr_microbench_mma_i8_pair": (i32, [i32, i32, i64, vp, vp]),
     "frr_rev_bits": (i32, [u64, u64, i64, i32, i32, vp, vp, vp]),
     "frr_launch_count": (ctypes.c_ulonglong, []),
     "frr_sim_pairs": (i32, [u64, u64, i64, i64, vp, vp, vp, vp]),

@@ -961,6 +961,89 @@ extern "C" int frr_microbench_mma_i8(int N, int a_tmem, int64_t iters, int64_t* 
     return frr_launched("k_microbench_mma");
 }
 
+namespace {
+// The same ceiling for CTA pairs: clusters of two CTAs on one TPC, the
+// leader issuing tcgen05.mma.cta_group::2.kind::i8 (M = 256: 128 rows per
+// CTA from its own shared memory or TMEM; B split by N, N/2 rows in each
+// CTA's shared memory; each CTA's TMEM holds its 128 x N accumulator).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_microbench_mma2(int N, int a_tmem, int64_t iters) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + BM * 128;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + (size_t)(N / 2) * 128);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (int o = threadIdx.x; o < (BM + N / 2) * 128 / 16; o += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[o] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint32_t a_lbo = (BM / 8) * 128, b_lbo = (uint32_t)(N / 16) * 128;
+        const uint32_t idesc = idesc_i8(2 * BM, N);
+        const uint64_t ad0 = umma_desc(smem_u32(sA), a_lbo, 128), bd0 = umma_desc(smem_u32(sB), b_lbo, 128);
+        for (int64_t it = 0; it < iters; it++) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) {
+                const uint64_t bd = bd0 + (uint64_t)((ks * 2 * b_lbo) >> 4);
+                const uint32_t acc = (it | ks) != 0;
+                if (a_tmem)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                        "r"(tmem + 256 + (uint32_t)(ks * 8)), "l"(bd), "r"(idesc), "r"(acc)
+                        : "memory");
+                else
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                        "l"(ad0 + (uint64_t)((ks * 2 * a_lbo) >> 4)), "l"(bd), "r"(idesc), "r"(acc)
+                        : "memory");
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(bar)),
+            "h"((uint16_t)3)
+            : "memory");
+    }
+    __syncwarp();
+    mbar_wait(bar, 0);
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if ((threadIdx.x >> 5) == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+}  // namespace
+
+extern "C" int frr_microbench_mma_i8_pair(int N, int a_tmem, int64_t iters, int64_t* ops_host, void* stream) {
+    if (N < 32 || N > 256 || N % 32 || iters < 1) {
+        frr_set_error("frr_microbench_mma_i8_pair: N must be 32..256 (multiple of 32), iters >= 1");
+        return FRR_E_INVALID_DESIGN;
+    }
+    const size_t smem = 1024 + (size_t)(BM + N / 2) * 128 + 64;
+    int rc = frr_prepare_kernel(k_microbench_mma2, smem);
+    if (rc) return rc;
+    const int grid = frr_num_sms() / 2 * 2;
+    k_microbench_mma2<<<grid, 128, smem, frr_stream(stream)>>>(N, a_tmem & 1, iters);
+    if (ops_host) *ops_host = (int64_t)(grid / 2) * iters * 4 * 2 * (2 * BM) * N * 32;
+    return frr_launched("k_microbench_mma2");
+}
+
 #if FRR_MMA_TIMING
 extern "C" int frr_debug_waits(unsigned long long* host16) {
     cudaDeviceSynchronize();
