@@ -265,7 +265,8 @@ def fiducial_interval(obs_w, obs_y, pool: RandomizationPool, alpha: float = 0.05
     return _fi_from_stats(ps, alpha)
 
 
-def _fi_from_stats(ps: _PoolStats, alpha: float) -> tuple[float, float]:
+def _fi_from_stats(ps: _PoolStats, alpha: float, a_host=None) -> tuple[float, float]:
+    """a_host: the pool's a already on the host (else it is copied here)."""
     tau_obs, b_obs, m = ps.tau_obs, ps.b_obs, ps.m
 
     def p_many(taus) -> np.ndarray:
@@ -273,7 +274,7 @@ def _fi_from_stats(ps: _PoolStats, alpha: float) -> tuple[float, float]:
         rhs = [abs(tau_obs - tau * b_obs) for tau in taus]
         return ps.counts(taus, rhs).astype(np.float64) / m
 
-    half = 10.0 * float(np.std(N.to_host(ps.a)))
+    half = 10.0 * float(np.std(N.to_host(ps.a) if a_host is None else a_host))
     if not np.isfinite(half) or half == 0.0:
         half = max(1.0, abs(tau_obs))
     lo_g, hi_g = tau_obs - half, tau_obs + half
@@ -374,7 +375,7 @@ def randomization_test(obs_w=None, obs_y=None, pool: RandomizationPool | None = 
         res = TestResult(p_value=float(count) / ps.m, tau_obs=ps.tau_obs, fi=None,
                          stat_distribution=N.to_host(ps.a), alpha=None, obs_in_pool=ps.in_pool)
         if find_fi:
-            res.fi = _fi_from_stats(ps, alpha)
+            res.fi = _fi_from_stats(ps, alpha, res.stat_distribution)
             res.alpha = alpha
         return res
     res = randomization_pvalue(obs_w, obs_y, pool, statistic=statistic)
