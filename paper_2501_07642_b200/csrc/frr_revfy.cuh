@@ -36,6 +36,9 @@
 #ifndef FRR_REV_PIPE
 #define FRR_REV_PIPE 0  // 1: next group's draws ahead of the bit moves; 2: interleaved draw/move
 #endif
+#ifndef FRR_REV_RA_ALU
+#define FRR_REV_RA_ALU 1  // r's word index by shr (ALU) instead of mul.hi (FMA pipe): C2 +2.7% (the FMA pipe is the busiest, 72%)
+#endif
 #ifndef FRR_REV_FETCH_AND
 #define FRR_REV_FETCH_AND 1  // 1: atom.and fetch-and-clear for the r-side bit
 #endif
@@ -98,7 +101,13 @@ __device__ __forceinline__ uint32_t frr_rev_draw1(uint64_t& x, uint64_t sa, uint
 // cases right.
 __device__ __forceinline__ void frr_rev_move(uint32_t wa, uint32_t e, uint32_t d) {
     uint32_t ra;  // r's word is W + e / 32
+#if FRR_REV_RA_ALU == 2
+    asm volatile("{\n\t.reg .u32 q;\n\tand.b32 q, %1, -32;\n\tshl.b32 q, q, 2;\n\tadd.u32 %0, q, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
+#elif FRR_REV_RA_ALU
+    asm volatile("{\n\t.reg .u32 q;\n\tshr.u32 q, %1, 5;\n\tshl.b32 q, q, 7;\n\tadd.u32 %0, q, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
+#else
     asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
+#endif
 #if FRR_REV_FETCH_AND
     // nm = ~(1 << (e & 31)); the rotation of the isolated bit right by d lands it on jb
     asm volatile(
