@@ -108,6 +108,12 @@ __host__ __device__ __forceinline__ StepC frr_make_step(int n, int k) {
 #ifndef FRR_MOD_Y_PAIR
 #define FRR_MOD_Y_PAIR 0
 #endif
+#ifndef FRR_MOD_Y_IMM0
+#define FRR_MOD_Y_IMM0 0
+#endif
+#ifndef FRR_MOD_R_IMM0
+#define FRR_MOD_R_IMM0 1  // madc.hi with an immediate zero: ptxas moves the addend copy to the ALU (C2 +0.2%)
+#endif
 __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s, uint32_t zero = 0u, uint32_t zero2 = 0u) {
     // written on 32-bit halves so the result stays a plain 32-bit register
     const uint32_t ulo = (uint32_t)u, uhi = (uint32_t)(u >> 32);
@@ -129,6 +135,9 @@ __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s, uin
     asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2));
     asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(ylo), "+r"(yhi) : "r"(ulo));
     (void)zero;
+#elif FRR_MOD_Y_IMM0
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo));
+    (void)zero;
 #else
     asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo), "r"(zero));
 #endif
@@ -137,9 +146,16 @@ __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s, uin
     const uint32_t lhi = __umulhi(mlo, ylo) + mhi * ylo + mlo * yhi;
     // result = floor(low * b / 2^64) = hi32(lhi * b + umulhi(llo, b))
     uint32_t rhi;  // the low word of the sum only feeds the carry
+#if FRR_MOD_R_IMM0
+    asm("{\n\t.reg .u32 rlo;\n\tmad.lo.cc.u32 rlo, %1, %2, %3;\n\tmadc.hi.u32 %0, %1, %2, 0;\n\t}"
+        : "=r"(rhi)
+        : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)));
+    (void)zero2;
+#else
     asm("{\n\t.reg .u32 rlo;\n\tmad.lo.cc.u32 rlo, %1, %2, %3;\n\tmadc.hi.u32 %0, %1, %2, %4;\n\t}"
         : "=r"(rhi)
         : "r"(lhi), "r"(s.b), "r"(__umulhi(llo, s.b)), "r"(zero2));
+#endif
     return rhi;
 }
 
