@@ -33,8 +33,11 @@ def _patch_compute(setattr_=setattr):
         bal = O.Balance(kernel._zq, kernel._inv_scale_sq)
         return torch.from_numpy(O.c_exact_stats(bal, design.n_treated, lo, count, threads=1))
 
-    def select(stats, lo, k, comm, keep_device=False):
+    def select(stats, lo, k, comm, keep_device=False, keys_seed=None):
         idx, val, thr = select_k_smallest(stats, lo, k, NumpySelectOps(), comm)
+        if keys_seed is not None:
+            keys = np.column_stack([np.full(idx.shape[0], keys_seed, dtype=np.uint64), idx.numpy().astype(np.uint64)])
+            return idx.numpy(), val.numpy(), thr, keys
         if keep_device:  # the "device" copy of the accepted ranks feeds exact_rows_device
             return idx.numpy(), val.numpy(), thr, idx.numpy().astype(np.uint64)
         return idx.numpy(), val.numpy(), thr
