@@ -5,7 +5,7 @@ the GPU path compared bit for bit with the C oracle (test infrastructure,
 multi-threaded on the host), and the accepted pools compared with the
 oracle's stable selection.
 
-    python tools/full_parity.py c2 [c4] [c5] > result.json"""
+    python tests/parity/full_parity.py c2 [c4] [c5] > result.json"""
 import json
 import os
 import sys
@@ -13,7 +13,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import oracle as O  # noqa: E402

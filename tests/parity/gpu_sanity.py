@@ -1,6 +1,6 @@
 """Quick on-GPU diagnosis of every libfrr entry point against the C oracle.
 Prints one line per check; never raises (so one failure does not hide the
-others).  Usage: python tools/gpu_sanity.py"""
+others).  Usage: python tests/parity/gpu_sanity.py"""
 
 import os
 import sys
@@ -9,7 +9,7 @@ import traceback
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 

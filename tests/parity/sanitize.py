@@ -1,7 +1,7 @@
 """Small invocations of every hot-path kernel family for compute-sanitizer
 (memcheck / racecheck / synccheck), each checked against the oracle:
 
-    compute-sanitizer --tool racecheck python tools/sanitize.py [case ...]
+    compute-sanitizer --tool racecheck python tests/parity/sanitize.py [case ...]
 
 cases: c1 (exact n=20 pool + test/FI), c2 (tensor-core Monte Carlo prefix,
 n=1000 d=64, 2^13 draws), c3 (N-tiled tensor-core prefix, n=2000 d=1024,
@@ -13,7 +13,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import oracle as O  # noqa: E402

@@ -1,5 +1,5 @@
 """Correctness + speed of one libfrr build (FRR_LIBRARY) on the C2 shape.
-Usage: FRR_LIBRARY=... python tools/variant_check.py [M]"""
+Usage: FRR_LIBRARY=... python tests/parity/variant_check.py [M]"""
 import os
 import sys
 import time
@@ -7,7 +7,7 @@ import time
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import oracle as O  # noqa: E402

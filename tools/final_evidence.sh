@@ -19,7 +19,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_mc
 M="dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,gpu__time_duration.sum"
 timeout 900 ncu --metrics $M --clock-control none -k regex:k_mc_stats_mma -s 1 -c 1 --csv --log-file $O/bench_kernel.csv \
     python tools/profile_mc.py 100000000 > $O/bench_kernel.log 2>&1
-for c in c2 c3 c4 c5; do timeout 900 python tools/full_parity.py $c > $O/full_parity_$c.json 2> $O/full_parity_$c.err; done
+for c in c2 c3 c4 c5; do timeout 900 python tests/parity/full_parity.py $c > $O/full_parity_$c.json 2> $O/full_parity_$c.err; done
 FRR_LIBRARY=tools/variants/libfrr_checks.so timeout 1500 python -m pytest tests -m gpu -q > $O/checks_gpu_tests.txt 2>&1
-FRR_LIBRARY=tools/variants/libfrr_checks.so timeout 900 python tools/sanitize.py > $O/checks_sanitize.txt 2>&1
+FRR_LIBRARY=tools/variants/libfrr_checks.so timeout 900 python tests/parity/sanitize.py > $O/checks_sanitize.txt 2>&1
 tail -1 $O/gpu_tests.txt $O/checks_gpu_tests.txt $O/smoke.txt
