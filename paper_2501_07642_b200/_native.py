@@ -199,21 +199,27 @@ _pool = {"free": [], "bytes": 0}
 
 
 class _PooledResult:
-    """Buffer exporter of one result: a byte range of a pooled slab."""
+    """Buffer exporter of one result: a byte range of a pooled slab.  The
+    slab goes back to the pool when the last exported view is released."""
 
-    __slots__ = ("slab", "nbytes")
+    __slots__ = ("slab", "nbytes", "views")
 
     def __init__(self, slab, nbytes):
         self.slab = slab
         self.nbytes = nbytes
+        self.views = 0
 
     def __buffer__(self, flags):
+        if self.slab is None:
+            raise BufferError("pooled result already released")
+        self.views += 1
         return memoryview(self.slab.numpy()[: self.nbytes])
 
     def __release_buffer__(self, view):
         view.release()
-        slab, self.slab = self.slab, None
-        if slab is not None:
+        self.views -= 1
+        if self.views == 0 and self.slab is not None:
+            slab, self.slab = self.slab, None
             with _pool_lock:
                 _pool["free"].append(slab)
 
