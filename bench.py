@@ -5,6 +5,9 @@ n=1000 units, 500 treated, d=64 Gaussian covariates, 1e8 candidates per
 GPU per step, prob_accept=1e-3.  One step = generate and balance-check
 every candidate (fused sm_100a kernel) + exact global acceptance selection
 (radix select + compaction; NCCL all-reduce of the histograms for N>1).
+The GPU runs the steps strictly one after another; the host enqueues step
+i+1's pass 1 (into a second statistics buffer) before it reads step i's
+selection back, so host-thread stalls shorter than a pass cost no GPU time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -113,6 +116,67 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+class NvmlStepSampler:
+    """Clocks and throttle reasons read through NVML (the library nvidia-smi
+    uses) from this process, once per step, right after the step's pass-1
+    kernel is launched: the query runs while the GPU is busy with that
+    kernel, so it cannot stall the step's later host syncs the way an
+    asynchronous nvidia-smi sample landing in the select does (measured: a
+    sample that lands there adds 1-10 ms, occasionally 60 ms, to a 100 ms
+    step).  Falls back to ClockSampler when pynvml is unavailable."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.handle = None
+        self.fallback = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            pr = torch.cuda.get_device_properties(self.index)
+            try:
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:  # noqa: BLE001
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.sample()
+        except Exception:  # noqa: BLE001
+            self.handle = None
+            self.fallback = ClockSampler(self.index).__enter__()
+        return self
+
+    def sample(self):
+        if self.handle is None:
+            return
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+
+    def __exit__(self, *a):
+        if self.fallback is not None:
+            self.fallback.__exit__(*a)
+            self.samples = self.fallback.samples
+            return
+        try:
+            self.nv.nvmlShutdown()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def summary(self):
+        out = ClockSampler.summary(self)
+        out["source"] = "nvidia-smi -lms" if self.fallback is not None else "NVML, once per timed step"
+        return out
+
+
 def _dist():
     import torch
     import torch.distributed as dist
@@ -209,7 +273,7 @@ def run_ours(args):
     import paper_2501_07642_b200 as frr
     from paper_2501_07642_b200 import _native as N
     from paper_2501_07642_b200 import generation as G
-    from paper_2501_07642_b200._select import DeviceSelectOps, TorchComm, LocalComm, select_k_smallest
+    from paper_2501_07642_b200._select import DeviceSelectOps, TorchComm, LocalComm, select_start
 
     rank, world, local = _dist()
     dev = torch.device("cuda", local)
@@ -226,63 +290,59 @@ def run_ours(args):
     ops = DeviceSelectOps()
     stream = torch.cuda.current_stream()
 
-    host_marks = []
-    step_traces = []
+    bufs = [stats, torch.empty_like(stats)]
 
-    def step(ev=None):
+    def launch_pass1(i, ev=None, clk=None):
         if ev:
             ev[0].record(stream)
-        G.mc_stats_device(kern, design, lo, hi - lo, out=stats)
+        G.mc_stats_device(kern, design, lo, hi - lo, out=bufs[i % 2])
         if ev:
             ev[1].record(stream)
-            host_marks.append(time.perf_counter())
-            if os.environ.get("FRR_BENCH_DEBUG"):
-                import paper_2501_07642_b200._select as SEL
+        if clk is not None:
+            clk.sample()  # while pass 1 runs (see NvmlStepSampler)
 
-                SEL.TRACE = []
-                step_traces.append(SEL.TRACE)
-        r = select_k_smallest(stats, lo, k, ops, comm)
-        if ev:
-            host_marks.append(time.perf_counter())
-        return r
+    def run_steps(n, evs=None, clk=None):
+        """n steps, each pass 1 over this GPU's candidates + the exact select.
+        The stream runs them strictly in order; the host enqueues the next
+        step's pass 1 (into the other statistics buffer) before it reads the
+        current step's select back, so a host thread that stalls for less than
+        a pass (~100 ms: seen on these VMs) leaves no gap on the GPU."""
+        launch_pass1(0, evs[0] if evs else None, clk)
+        job = select_start(bufs[0], lo, k, ops, comm, m_total=total)
+        res = None
+        for i in range(n):
+            if i + 1 < n:
+                launch_pass1(i + 1, evs[i + 1] if evs else None, clk)
+            res = job.finish()
+            if i + 1 < n:
+                job = select_start(bufs[(i + 1) % 2], lo, k, ops, comm, m_total=total)
+        return res
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     # no interpreter garbage collection inside the timed region (as timeit
     # does): a collection pass stalls the host between the select's kernels
     import gc
 
     gc.collect()
     gc.disable()
-    with ClockSampler(local) as clk:
-        # warm-up under the same conditions as the timed steps (sampler
-        # running, collector off): the first steps after those start showed
-        # a one-off host stall of 2-100 ms
-        for _ in range(args.warmup):
-            step()
+    with NvmlStepSampler(local) as clk:
+        # warm-up under the same conditions as the timed steps
+        run_steps(args.warmup, clk=clk)
         torch.cuda.synchronize()
         _barrier(world)
         torch.cuda.synchronize()
         launches0 = int(N.lib().frr_launch_count())
         t_start.record(stream)
-        marks[0].record(stream)
-        for i in range(args.steps):
-            res = step(evs[i])
-            marks[i + 1].record(stream)
+        res = run_steps(args.steps, evs, clk)
         t_end.record(stream)
         launches = int(N.lib().frr_launch_count()) - launches0  # libfrr kernels of the timed region
         torch.cuda.synchronize()
     gc.enable()
     if os.environ.get("FRR_BENCH_DEBUG"):
-        print("steps ms:", [round(marks[i].elapsed_time(marks[i + 1]), 2) for i in range(args.steps)],
-              "pass1 ms:", [round(a.elapsed_time(b), 2) for a, b in evs],
-              "host select ms:", [round(1e3 * (host_marks[2 * i + 1] - host_marks[2 * i]), 1) for i in range(args.steps)],
+        print("pass1 ms:", [round(a.elapsed_time(b), 2) for a, b in evs],
+              "gaps ms:", [round(evs[i][1].elapsed_time(evs[i + 1][0]), 2) for i in range(args.steps - 1)],
               file=sys.stderr)
-        for i, tr in enumerate(step_traces):
-            t0 = host_marks[2 * i]
-            print(f"step {i} select trace (ms after pass-1 launch):",
-                  " ".join(f"{lab}={1e3 * (t - t0):.1f}" for lab, t in tr), file=sys.stderr)
     _barrier(world)
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end) / args.steps

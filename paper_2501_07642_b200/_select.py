@@ -19,6 +19,7 @@ accepted-key gather.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -69,6 +70,11 @@ class DeviceSelectOps:
     def set_threshold(self, st, bits: int):
         """State whose threshold is the given bit pattern (all 64 bits fixed)."""
         st[0] = int(np.array([bits], dtype=np.uint64).view(np.int64)[0])
+        st[1] = -1
+
+    def set_threshold_from(self, st, src):
+        """set_threshold with the bit pattern of src's threshold, on the device."""
+        st[0:1].copy_(src[0:1])
         st[1] = -1
 
     def threshold(self, st) -> float:
@@ -176,16 +182,23 @@ def bound_from_sample(sample, k: int, m_total: int, ops, comm):
         sample = torch.cat([sample, sample.new_full((s_r - sample.shape[0],), float("inf"))])
     if comm.world > 1:
         sample = torch.cat(comm.all_gather(sample))
+    st, frac = _bound_state(sample, k, m_total, ops)
+    _mark("bound launched")
+    h = int(st[0].item()) & ((1 << 64) - 1)
+    _mark("bound read")
+    return h, frac
+
+
+def _bound_state(sample, k: int, m_total: int, ops):
+    """Select state whose threshold (st[0]) is the bound h of the gathered
+    sample, left on the device; and the sampled fraction k_s / s."""
     s = int(sample.shape[0])
     qs = k / m_total * s
     k_s = min(s, int(math.ceil(qs + 8.0 * math.sqrt(qs) + 16)))
     st = ops.init(k_s, sample.device)
     for p in range(8):
         ops.pick(ops.hist(sample, st, p), st, p)
-    _mark("bound launched")
-    h = int(st[0].item()) & ((1 << 64) - 1)
-    _mark("bound read")
-    return h, k_s / s
+    return st, k_s / s
 
 
 def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool = True):
@@ -200,41 +213,95 @@ def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool
     sample), then runs the radix passes and the final compaction on C: two
     passes over the full statistics instead of ten.  Every statistic <= the
     threshold is in C, so the result is the same as on the full data."""
+    return select_start(stats, index_base, k, ops, comm, prefilter).finish()
+
+
+class SelectJob:
+    """A select whose kernels are all enqueued; finish() reads the result
+    back (the only host synchronisation) and, if the narrowing failed, runs
+    the select on the full statistics.  The statistics must stay unchanged
+    until finish() returns."""
+
+    def __init__(self, finish):
+        self._finish = finish
+
+    def finish(self):
+        return self._finish()
+
+
+def select_start(stats, index_base: int, k: int, ops, comm, prefilter: bool = True, m_total=None) -> SelectJob:
+    """Enqueue the select of select_k_smallest without waiting for it
+    (m_total: the global statistics count when the caller knows it, which
+    saves a collective and its host read)."""
     torch = N.torch_mod()
-    m_total = int(stats.shape[0])
-    if comm.world > 1:
-        mt = torch.tensor([m_total], dtype=torch.int64, device=stats.device)
-        m_total = int(comm.all_reduce_(mt).item())
+    if m_total is None:
+        m_total = int(stats.shape[0])
+        if comm.world > 1:
+            mt = torch.tensor([m_total], dtype=torch.int64, device=stats.device)
+            m_total = int(comm.all_reduce_(mt).item())
+    if os.environ.get("FRR_SELECT_PREFILTER") == "0":  # A/B knob
+        prefilter = False
     if prefilter and m_total >= PREFILTER_MIN and k <= PREFILTER_MAX_Q * m_total:
-        h, qh = _upper_bound_bits(stats, k, m_total, ops, comm)
-        sth = ops.init(k, stats.device)
-        ops.set_threshold(sth, h)
-        everything = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=stats.device)
+        # Every kernel of the narrowed select is enqueued without a host
+        # round trip (the bound, the narrowed count and the tie quota stay
+        # on the device), so a host thread that stalls while they run costs
+        # no GPU time: the narrowed buffer's unused tail holds +inf, which
+        # never enters a selection of k <= count finite statistics.  The
+        # two ways the narrowing can fail -- a capped buffer that overflowed
+        # or fewer than k statistics under the bound -- are checked once at
+        # the end and fall back to the select on the full data.
         m = int(stats.shape[0])
+        s_r = sample_size(m, comm)
+        sample = stats[:: max(1, m // s_r)][:s_r].contiguous()
+        if comm.world > 1:
+            r_s = SAMPLE // comm.world
+            if sample.shape[0] < r_s:  # keep shapes equal across ranks
+                sample = torch.cat([sample, sample.new_full((r_s - sample.shape[0],), float("inf"))])
+            sample = torch.cat(comm.all_gather(sample))
+        st_h, qh = _bound_state(sample, k, m_total, ops)
+        sth = ops.init(k, stats.device)
+        ops.set_threshold_from(sth, st_h)
+        everything = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=stats.device)
         cap = int(qh * m * 1.25) + 4096
         c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, cap)
         _mark("compact launched")
-        n_c = int(c_n.item())
-        _mark("compact read")
-        if n_c > c_idx.shape[0]:
-            c_idx, c_val, c_n = ops.compact(stats, index_base, sth, everything, n_c)
+        pos = torch.arange(c_val.shape[0], device=c_val.device)
+        c_val = c_val.masked_fill(pos >= c_n, float("inf"))
+        over = (c_n > c_val.shape[0]).to(torch.int64)
         tot = c_n.clone()
         if comm.world > 1:
+            comm.all_reduce_(over)
             comm.all_reduce_(tot)
-        if int(tot.item()) >= k:
-            return _select_full(c_val[:n_c].contiguous(), 0, k, ops, comm, idx_map=c_idx[:n_c])
-    return _select_full(stats, index_base, k, ops, comm)
+        job = _full_start(c_val, 0, k, ops, comm, idx_map=c_idx)
+
+        def finish():
+            if int(over.item()) == 0 and int(tot.item()) >= k:
+                res = _full_finish(job, comm)
+                _mark("narrowed ok")
+                return res
+            return _full_finish(_full_start(stats, index_base, k, ops, comm), comm)
+
+        return SelectJob(finish)
+    job = _full_start(stats, index_base, k, ops, comm)
+    return SelectJob(lambda: _full_finish(job, comm))
 
 
 def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
     """The radix select proper; idx_map (narrowed input) maps local positions
     to global indices before the gather."""
+    return _full_finish(_full_start(stats, index_base, k, ops, comm, idx_map), comm)
+
+
+def _full_start(stats, index_base: int, k: int, ops, comm, idx_map=None):
+    """Enqueue the radix passes and the final compaction (no host read)."""
     torch = N.torch_mod()
     st = ops.init(k, stats.device)
+    _mark("full init")
     for p in range(8):
         h = ops.hist(stats, st, p)
         comm.all_reduce_(h)
         ops.pick(h, st, p)
+    _mark("full hist")
     if comm.world == 1:
         quota = ops.k_rem(st)
     else:
@@ -246,6 +313,13 @@ def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
         quota = torch.minimum(quota, eq[comm.rank : comm.rank + 1]).contiguous()
     idx, val, n_out = ops.compact(stats, index_base, st, quota, cap=k)
     _mark("final launched")
+    return idx, val, n_out, st, ops, idx_map
+
+
+def _full_finish(job, comm):
+    """Read back the select enqueued by _full_start: (indices, values, threshold)."""
+    torch = N.torch_mod()
+    idx, val, n_out, st, ops, idx_map = job
     thr = ops.threshold(st)
     _mark("final read")
     if idx_map is not None:

@@ -35,7 +35,7 @@ constexpr int BM = 128;        // candidates per tile = MMA M
 #define FRR_MMA_TW 1  // 2 measured -2% (20 generators + 8 tile warps vs 24 + 4)
 #endif
 #ifndef FRR_MMA_NFY
-#define FRR_MMA_NFY (FRR_MMA_TW == 2 ? 20 : 26)
+#define FRR_MMA_NFY 20  // the launch bound: 28 warps -> 72 registers per thread (26: 32 warps, 64)
 #endif
 #ifndef FRR_MMA_KC
 #define FRR_MMA_KC 64
@@ -68,7 +68,7 @@ constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: the
 // every 8-group: numpy's accumulator streams r0-3 / r4-7, joined through
 // shared memory)
 #ifndef FRR_MMA_RFY
-#define FRR_MMA_RFY (FRR_MMA_TW == 2 ? 20 : 24)
+#define FRR_MMA_RFY 20  // 20 generators at 72 registers beat 24 at 64 by 1% (16 at 80: -1.7%)
 #endif
 #ifndef FRR_MMA_RBITS
 #define FRR_MMA_RBITS 8

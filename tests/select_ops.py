@@ -51,5 +51,9 @@ class NumpySelectOps:
         st[0] = int(np.array([bits], dtype=np.uint64).view(np.int64)[0])
         st[1] = -1
 
+    def set_threshold_from(self, st, src):
+        st[0] = src[0]
+        st[1] = -1
+
     def threshold(self, st):
         return float(np.array([int(st[0]) & (2**64 - 1)], dtype=np.uint64).view(np.float64)[0])

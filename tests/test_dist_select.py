@@ -25,8 +25,16 @@ def _worker(rank, world, port, stats, p, out, narrow="off"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     if narrow != "off":  # exercise the sampled narrowing (and its fall back) at test sizes
         S.PREFILTER_MIN, S.SAMPLE, S.PREFILTER_MAX_Q = 1, 512, 1.0
-        if narrow == "bad-bound":
-            S._upper_bound_bits = lambda *a: (0, 0.0)
+        if narrow == "bad-bound":  # h = +0.0: fewer than k statistics under the bound
+            def low(sample, k, m_total, ops):
+                st = ops.init(1, sample.device)
+                ops.set_threshold(st, 0)
+                return st, 0.0
+
+            S._bound_state = low
+        if narrow == "overflow":  # the true bound with a zero fraction: the capped buffer overflows
+            true_state = S._bound_state
+            S._bound_state = lambda *a: (true_state(*a)[0], 0.0)
     try:
         M = stats.shape[0]
         lo, hi = M * rank // world, M * (rank + 1) // world
@@ -46,7 +54,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world,ties,p,narrow", [(2, True, 0.1, "off"), (2, False, 0.01, "off"), (3, True, 0.37, "off"),
                                                  (2, False, 0.01, "on"), (3, True, 0.05, "on"),
-                                                 (2, True, 0.02, "bad-bound")])
+                                                 (2, True, 0.02, "bad-bound"), (3, False, 0.05, "overflow")])
 def test_distributed_select_matches_stable_sort(world, ties, p, narrow):
     rng = np.random.default_rng(world * 7 + ties)
     M = 20011

@@ -109,12 +109,52 @@ def test_select_vs_oracle(M, p, ties):
 
 def test_narrowing_fallback_when_bound_is_low(monkeypatch):
     from paper_2501_07642_b200 import _select as S
-    monkeypatch.setattr(S, "_upper_bound_bits", lambda *a: (0, 0.0))  # h = +0.0: far too low
+
+    def low(sample, k, m_total, ops):  # h = +0.0: far too low
+        st = ops.init(1, sample.device)
+        ops.set_threshold(st, 0)
+        return st, 0.0
+
+    monkeypatch.setattr(S, "_bound_state", low)
     rng = np.random.default_rng(5)
     st = rng.random(5_000_000) + 0.5
     acc, thr = G._select(st, 1e-3)
     want, wthr = O.c_select(st, 1e-3)
     assert np.array_equal(acc, want) and thr == wthr
+
+
+def test_narrowing_fallback_when_buffer_overflows(monkeypatch):
+    """The true bound with a zero sampled fraction: the capped narrowing
+    buffer (4096 entries) overflows, detected at the end of the select."""
+    from paper_2501_07642_b200 import _select as S
+
+    true_state = S._bound_state
+    monkeypatch.setattr(S, "_bound_state", lambda *a: (true_state(*a)[0], 0.0))
+    rng = np.random.default_rng(6)
+    st = rng.random(5_000_000)
+    acc, thr = G._select(st, 1e-2)
+    want, wthr = O.c_select(st, 1e-2)
+    assert np.array_equal(acc, want) and thr == wthr
+
+
+def test_narrowed_select_has_no_host_sync_before_the_end(monkeypatch):
+    """The narrowed select reads nothing back until every kernel is queued
+    (host stalls during the select then cost no GPU time)."""
+    import torch
+
+    from paper_2501_07642_b200 import _select as S
+    from paper_2501_07642_b200._select import DeviceSelectOps, LocalComm
+
+    rng = np.random.default_rng(7)
+    stats = torch.from_numpy(rng.random(8_000_000)).cuda()
+    S.TRACE = []
+    try:
+        S.select_k_smallest(stats, 0, 8000, DeviceSelectOps(), LocalComm())
+        labels = [lab for lab, _ in S.TRACE]
+    finally:
+        S.TRACE = None
+    assert "bound read" not in labels and "compact read" not in labels
+    assert labels.index("final launched") < labels.index("narrowed ok")
 
 
 def test_capped_compaction_reports_full_count():
