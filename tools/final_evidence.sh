@@ -22,4 +22,4 @@ timeout 900 ncu --metrics $M --clock-control none -k regex:k_mc_stats_mma -s 1 -
 for c in c2 c3 c4 c5; do timeout 900 python tests/parity/full_parity.py $c > $O/full_parity_$c.json 2> $O/full_parity_$c.err; done
 FRR_LIBRARY=tools/variants/libfrr_checks.so timeout 1500 python -m pytest tests -m gpu -q > $O/checks_gpu_tests.txt 2>&1
 FRR_LIBRARY=tools/variants/libfrr_checks.so timeout 900 python tests/parity/sanitize.py > $O/checks_sanitize.txt 2>&1
-tail -1 $O/gpu_tests.txt $O/checks_gpu_tests.txt $O/smoke.txt
+for f in gpu_tests.txt checks_gpu_tests.txt smoke.txt; do tail -n 1 $O/$f; done
