@@ -102,15 +102,6 @@ __host__ __device__ __forceinline__ StepC frr_make_step(int n, int k) {
     return s;
 }
 
-#ifndef FRR_MOD_Y_ADD
-#define FRR_MOD_Y_ADD 0
-#endif
-#ifndef FRR_MOD_Y_PAIR
-#define FRR_MOD_Y_PAIR 0
-#endif
-#ifndef FRR_MOD_Y_IMM0
-#define FRR_MOD_Y_IMM0 0
-#endif
 #ifndef FRR_MOD_R_IMM0
 #define FRR_MOD_R_IMM0 1  // madc.hi with an immediate zero: ptxas moves the addend copy to the ALU (C2 +0.2%)
 #endif
@@ -119,28 +110,7 @@ __device__ __forceinline__ uint32_t frr_mod_step(uint64_t u, const StepC& s, uin
     const uint32_t ulo = (uint32_t)u, uhi = (uint32_t)(u >> 32);
     const uint32_t mlo = (uint32_t)s.M, mhi = (uint32_t)(s.M >> 32);
     uint32_t ylo, yhi;  // y = uhi * c2 + ulo  (< 2^48)
-#if FRR_MOD_Y_PAIR
-    // y + uhi 2^32 = uhi c2 + u with u's own register pair as the addend,
-    // then uhi off the high word (mod 2^32; y < 2^48): no zero-pair copy
-    {
-        uint64_t yw;
-        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yw) : "r"(uhi), "r"(s.c2), "l"(u));
-        ylo = (uint32_t)yw;
-        yhi = (uint32_t)(yw >> 32) - uhi;
-        (void)zero;
-    }
-#elif FRR_MOD_Y_ADD
-    // the product on the FMA pipe, the addition on the ALU (no zero-pair
-    // register copy for a 64-bit addend)
-    asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2));
-    asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(ylo), "+r"(yhi) : "r"(ulo));
-    (void)zero;
-#elif FRR_MOD_Y_IMM0
-    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo));
-    (void)zero;
-#else
     asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;" : "=r"(ylo), "=r"(yhi) : "r"(uhi), "r"(s.c2), "r"(ulo), "r"(zero));
-#endif
     // low = M * y mod 2^64
     const uint32_t llo = mlo * ylo;
     const uint32_t lhi = __umulhi(mlo, ylo) + mhi * ylo + mlo * yhi;

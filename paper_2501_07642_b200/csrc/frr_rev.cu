@@ -10,10 +10,6 @@
 #include "frr_launch.cuh"
 #include "frr_revfy.cuh"
 
-#ifndef FRR_REV_BATCH
-#define FRR_REV_BATCH 0  // 1: batched bit moves per group (frr_rev_move_group; bit-exact, measured 7% slower at n = 5000)
-#endif
-
 namespace {
 constexpr int kRevWarps = 16;
 
@@ -75,7 +71,7 @@ __global__ void __launch_bounds__(kRevWarps * 32) k_rev_bits(uint64_t seed, cons
         const int64_t c = job * 32 + lane;
         const uint64_t state =
             frr_derive_state(seed, ids ? ids[c < count ? c : count - 1] : lo + (uint64_t)c);
-        const bool flag = frr_rev_fy<GS, FRR_REV_BATCH>(state, t, sst, wsa, P.kw);
+        const bool flag = frr_rev_fy<GS>(state, t, sst, wsa, P.kw);
         uint32_t fl = __ballot_sync(FRR_FULL, flag);
         while (fl) {
             const int src = __ffs(fl) - 1;

@@ -101,9 +101,7 @@ __device__ __forceinline__ uint32_t frr_rev_draw1(uint64_t& x, uint64_t sa, uint
 // cases right.
 __device__ __forceinline__ void frr_rev_move(uint32_t wa, uint32_t e, uint32_t d) {
     uint32_t ra;  // r's word is W + e / 32
-#if FRR_REV_RA_ALU == 2
-    asm volatile("{\n\t.reg .u32 q;\n\tand.b32 q, %1, -32;\n\tshl.b32 q, q, 2;\n\tadd.u32 %0, q, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
-#elif FRR_REV_RA_ALU
+#if FRR_REV_RA_ALU
     asm volatile("{\n\t.reg .u32 q;\n\tshr.u32 q, %1, 5;\n\tshl.b32 q, q, 7;\n\tadd.u32 %0, q, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
 #else
     asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
@@ -132,46 +130,6 @@ __device__ __forceinline__ void frr_rev_move(uint32_t wa, uint32_t e, uint32_t d
         "r"(e), "r"(wa), "r"(d)
         : "memory");
 #endif
-}
-
-// All FRR_REV_GROUP bit moves of one group at once (BATCH generators).
-// The group's steps j_i = 32 W + jb_i, jb_i = jtop - i, all write bits of
-// word W (address wa).  Their fetch-and-clears go out back to back (no
-// atomic waits for the one before it) and one OR stores the group's bits.
-// A step i whose source r_i is the target j_k of an earlier step k of the
-// same group (d_i in [1, i]: r_i = j_i + d_i = j_{i - d_i}) would read bit
-// j_k before that OR -- it reads 0 (bit j_k is untouched before step k)
-// and takes the bit from the register word V instead, clearing it there.
-// Sources in other words, above the group or repeated are seen in program
-// order by the atomics themselves.
-__device__ __forceinline__ void frr_rev_move_group(uint32_t wa, int jtop, const uint32_t (&dd)[FRR_REV_GROUP]) {
-    uint32_t c[FRR_REV_GROUP];
-#pragma unroll
-    for (int i = 0; i < FRR_REV_GROUP; i++) {
-        const uint32_t e = (uint32_t)(jtop - i) + dd[i];
-        uint32_t ra;
-        asm("{\n\t.reg .u32 q;\n\tmul.hi.u32 q, %1, 0x8000000;\n\tmad.lo.u32 %0, q, 128, %2;\n\t}" : "=r"(ra) : "r"(e), "r"(wa));
-        asm volatile(
-            "{\n\t.reg .u32 w, nm;\n\t"
-            "shf.l.wrap.b32 nm, %3, %3, %2;\n\t"
-            "atom.shared.and.b32 w, [%1], nm;\n\t"
-            "lop3.b32 %0, w, nm, 0, 0x30;\n\t}"  // w & ~nm: the source bit, in place
-            : "=r"(c[i])
-            : "r"(ra), "r"(e), "r"(0xFFFFFFFEu)
-            : "memory");
-    }
-    uint32_t V = 0;
-#pragma unroll
-    for (int i = 0; i < FRR_REV_GROUP; i++) {
-        const uint32_t d = dd[i];
-        uint32_t v;
-        asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(v) : "r"(c[i]), "r"(d));
-        // hazard: source = target of step i - d of this group (bit jtop - i + d of V)
-        const uint32_t m = (d - 1u < (uint32_t)i) ? (1u << ((uint32_t)(jtop - i) + d)) : 0u;
-        const uint32_t b = V & m;
-        V = (V ^ b) | (b >> d) | v;
-    }
-    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wa), "r"(V) : "memory");
 }
 
 // FRR_REV_GROUP draws of consecutive steps (descending j from the record at
@@ -208,7 +166,7 @@ __device__ __forceinline__ void frr_rev_draws(uint64_t& x, uint64_t sa, uint32_t
 // ahead of the current group's bit moves, so their independent register
 // work fills the latency of the serial shared-memory chain (each move's
 // atomic must return before its OR).
-template <bool GS = false, bool BATCH = false>
+template <bool GS = false>
 __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps, uint32_t wsa, int kw) {
     constexpr int GPW = 32 / FRR_REV_GROUP;  // groups per 32-step word block
     const int wtop = (t - 1) >> 5;
@@ -260,15 +218,11 @@ __device__ __forceinline__ bool frr_rev_fy(uint64_t state, int t, uint64_t steps
                 if (more) sa -= 16ull * FRR_REV_GROUP;
                 continue;
             }
-            if (BATCH) {
-                frr_rev_move_group(wa, 31 - q * FRR_REV_GROUP, dd);
-            } else {
 #pragma unroll
-                for (int i = 0; i < FRR_REV_GROUP; i++) {
-                    const int jb = 31 - q * FRR_REV_GROUP - i;
-                    FRR_CHECK(32 * W + jb + (int)dd[i] < 32 * kw);  // r inside this lane's bitset
-                    frr_rev_move(wa, (uint32_t)jb + dd[i], dd[i]);
-                }
+            for (int i = 0; i < FRR_REV_GROUP; i++) {
+                const int jb = 31 - q * FRR_REV_GROUP - i;
+                FRR_CHECK(32 * W + jb + (int)dd[i] < 32 * kw);  // r inside this lane's bitset
+                frr_rev_move(wa, (uint32_t)jb + dd[i], dd[i]);
             }
             if (!FRR_REV_PIPE && (q < GPW - 1 || W > 0)) {
                 frr_rev_draws<GS>(x, sa, z0, z1, dn, hmax);
