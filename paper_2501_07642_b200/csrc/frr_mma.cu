@@ -73,6 +73,9 @@ constexpr int NFY = FRR_MMA_NFY;  // max generator warps (fewer for large n: the
 #ifndef FRR_MMA_RBITS
 #define FRR_MMA_RBITS 8
 #endif
+#ifndef FRR_MMA_SPARE
+#define FRR_MMA_SPARE 2  // tile buffers beyond the RFY / 4 being built
+#endif
 constexpr int RFY = FRR_MMA_RFY;
 constexpr int TW2 = FRR_MMA_TW;
 static_assert(TW2 == 1 || TW2 == 2, "tile warps per quadrant");
@@ -204,7 +207,7 @@ __host__ __device__ inline MmaShape mma_shape(int n, int t, int d, int L) {
     s.gen = 1;
     s.steps_smem = 1;
     for (int f = RFY; f >= 8; f -= 4) {
-        const int nb = f / 4 + 2 <= RBITS ? f / 4 + 2 : RBITS;
+        const int nb = f / 4 + FRR_MMA_SPARE <= RBITS ? f / 4 + FRR_MMA_SPARE : RBITS;
         set_roles(s, f, nb);
         if (smem_plan(s).total <= 227 * 1024) return s;
     }
