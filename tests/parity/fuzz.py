@@ -7,7 +7,9 @@ it (tensor-core single pass / N-tiled / CUDA-core by FRR_MC_PATH):
   exact  exact-enumeration statistics of a random rank window (small n);
   regen  key -> assignment regeneration of random draws;
   dim    the randomization-test statistic a of random keys (thread-per-key
-         stream path, frr_dim_mc_ws) for a random outcome vector.
+         stream path, frr_dim_mc_ws) for a random outcome vector;
+  select the exact acceptance select (sampled narrowing above 2^22
+         statistics) on random statistics with ties and zeros.
 
     python tests/parity/fuzz.py [seconds] [seed] > fuzz.json
 prints one JSON summary line (cases per kind, mismatching cases listed)."""
@@ -96,12 +98,24 @@ def case_dim(rng):
     return ok, dict(n=n, t=t, seed=seed, m=m)
 
 
+def case_select(rng):
+    M = int(rng.choice([int(rng.integers(1000, 200_000)), int(rng.integers(4_200_000, 7_000_000))]))
+    p = float(rng.choice([1e-4, 1e-3, 1e-2, 0.05, float(rng.uniform(1e-5, 0.2))]))
+    ties = bool(rng.integers(0, 2))
+    st = np.round(rng.random(M) * (7 if ties else 1e12)) / 3.0
+    st[: int(rng.integers(0, M // 5 + 1))] = 0.0
+    st = rng.permutation(st)
+    acc, thr = G._select(st, p)
+    want, wthr = O.c_select(st, p)
+    return bool(np.array_equal(acc, want) and thr == wthr), dict(M=M, p=p, ties=ties)
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2026)
     t_end = time.time() + budget
     counts, bad, routes = {}, [], {}
-    kinds = ["mc_auto", "mc_cuda_core", "exact", "regen", "dim"]
+    kinds = ["mc_auto", "mc_cuda_core", "exact", "regen", "dim", "select"]
     i = 0
     while time.time() < t_end:
         kind = kinds[i % len(kinds)]
@@ -114,8 +128,10 @@ def main():
             ok, info = case_exact(rng)
         elif kind == "regen":
             ok, info = case_regen(rng)
-        else:
+        elif kind == "dim":
             ok, info = case_dim(rng)
+        else:
+            ok, info = case_select(rng)
         counts[kind] = counts.get(kind, 0) + 1
         if kind.startswith("mc"):
             r = "cuda_core" if kind == "mc_cuda_core" else {0: "cuda_core", 1: "tcgen05 single", 2: "tcgen05 N-tiled"}[
