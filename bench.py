@@ -5,9 +5,10 @@ n=1000 units, 500 treated, d=64 Gaussian covariates, 1e8 candidates per
 GPU per step, prob_accept=1e-3.  One step = generate and balance-check
 every candidate (fused sm_100a kernel) + exact global acceptance selection
 (radix select + compaction; NCCL all-reduce of the histograms for N>1).
-The GPU runs the steps strictly one after another; the host enqueues step
-i+1's pass 1 (into a second statistics buffer) before it reads step i's
-selection back, so host-thread stalls shorter than a pass cost no GPU time.
+The GPU runs the steps strictly one after another; the host keeps up to 4
+steps enqueued (each with its own statistics buffer) and reads a step's
+selection back only before its buffer is reused, so host-thread stalls
+shorter than three passes cost no GPU time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -290,32 +291,48 @@ def run_ours(args):
     ops = DeviceSelectOps()
     stream = torch.cuda.current_stream()
 
-    bufs = [stats, torch.empty_like(stats)]
+    # statistics buffers in flight: the host may stall for up to (depth - 1)
+    # passes (~100 ms each) without leaving the GPU idle
+    depth = max(2, int(os.environ.get("FRR_BENCH_DEPTH", "4")))
+    bufs = [stats] + [torch.empty_like(stats) for _ in range(depth - 1)]
 
     def launch_pass1(i, ev=None, clk=None):
         if ev:
             ev[0].record(stream)
-        G.mc_stats_device(kern, design, lo, hi - lo, out=bufs[i % 2])
+        G.mc_stats_device(kern, design, lo, hi - lo, out=bufs[i % depth])
         if ev:
             ev[1].record(stream)
         if clk is not None:
             clk.sample()  # while pass 1 runs (see NvmlStepSampler)
 
-    def run_steps(n, evs=None, clk=None):
+    def run_steps(n, evs=None, clk=None, end_ev=None):
         """n steps, each pass 1 over this GPU's candidates + the exact select.
-        The stream runs them strictly in order; the host enqueues the next
-        step's pass 1 (into the other statistics buffer) before it reads the
-        current step's select back, so a host thread that stalls for less than
-        a pass (~100 ms: seen on these VMs) leaves no gap on the GPU."""
-        launch_pass1(0, evs[0] if evs else None, clk)
-        job = select_start(bufs[0], lo, k, ops, comm, m_total=total)
-        res = None
+        The stream runs them strictly in order.  The host keeps up to `depth`
+        steps enqueued (each in its own statistics buffer) and reads a step's
+        selection back only before its buffer is reused, so a host thread
+        that stalls for less than depth - 1 passes (seen on these VMs: 10 ms
+        to over 100 ms) leaves no gap on the GPU."""
+        from collections import deque
+
+        jobs, res = deque(), None
+        dbg = [] if (evs and os.environ.get("FRR_BENCH_DEBUG")) else None
         for i in range(n):
-            if i + 1 < n:
-                launch_pass1(i + 1, evs[i + 1] if evs else None, clk)
-            res = job.finish()
-            if i + 1 < n:
-                job = select_start(bufs[(i + 1) % 2], lo, k, ops, comm, m_total=total)
+            t0 = time.perf_counter()
+            if len(jobs) == depth:
+                res = jobs.popleft().finish()  # before pass 1 overwrites its buffer
+            t1 = time.perf_counter()
+            launch_pass1(i, evs[i] if evs else None, clk)
+            t2 = time.perf_counter()
+            jobs.append(select_start(bufs[i % depth], lo, k, ops, comm, m_total=total))
+            if dbg is not None:
+                dbg.append((round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
+                            round(1e3 * (time.perf_counter() - t2), 1)))
+        if dbg is not None:
+            print("host ms per step (finish, pass-1 launch, select enqueue):", dbg, file=sys.stderr)
+        if end_ev is not None:
+            end_ev.record(stream)  # the GPU reaches it when the last select is done
+        while jobs:
+            res = jobs.popleft().finish()
         return res
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -333,9 +350,18 @@ def run_ours(args):
         _barrier(world)
         torch.cuda.synchronize()
         launches0 = int(N.lib().frr_launch_count())
+        import paper_2501_07642_b200._select as SEL
+
+        fallbacks0 = SEL.FALLBACKS
+        t_last = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        res = run_steps(args.steps, evs, clk)
+        res = run_steps(args.steps, evs, clk, end_ev=t_last)
         t_end.record(stream)
+        if SEL.FALLBACKS == fallbacks0:
+            # no select fell back (which enqueues more work during the reads):
+            # the timed region ends where the GPU finished the last select, not
+            # where the host got round to recording an event after its reads
+            t_end = t_last
         launches = int(N.lib().frr_launch_count()) - launches0  # libfrr kernels of the timed region
         torch.cuda.synchronize()
     gc.enable()
@@ -356,11 +382,14 @@ def run_ours(args):
     frr.monte_carlo_pool(X, design)  # warm-up (first-call kernel attributes, allocator)
     _barrier(world)
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()  # as in the timed region (and timeit)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         pool = frr.monte_carlo_pool(X, design)
     torch.cuda.synchronize()
     e2e_s = _max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
+    gc.enable()
     h2d = N_UNITS * D_COV * 8 + 2 * D_COV * 8 + 8 * 16  # Zq, colsum, cc, (seeds/state)
     d2h = pool.n_accepted * 16 + 8 * 4  # accepted draw indices + stats, threshold/count
     assert pool.n_accepted == k and n_acc == k

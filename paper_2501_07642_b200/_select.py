@@ -67,15 +67,17 @@ class DeviceSelectOps:
                N.ptr(idx), N.ptr(val), N.ptr(n_out), N.ptr(ws), N.stream_ptr())
         return idx, val, n_out
 
+    # (fill_ with a Python scalar is a device fill; `st[1] = -1` would be a
+    # blocking host-to-device copy that waits for everything queued before it)
     def set_threshold(self, st, bits: int):
         """State whose threshold is the given bit pattern (all 64 bits fixed)."""
-        st[0] = int(np.array([bits], dtype=np.uint64).view(np.int64)[0])
-        st[1] = -1
+        st[0:1].fill_(int(np.array([bits], dtype=np.uint64).view(np.int64)[0]))
+        st[1:2].fill_(-1)
 
     def set_threshold_from(self, st, src):
         """set_threshold with the bit pattern of src's threshold, on the device."""
         st[0:1].copy_(src[0:1])
-        st[1] = -1
+        st[1:2].fill_(-1)
 
     def threshold(self, st) -> float:
         bits = int(st[0].item()) & ((1 << 64) - 1)
@@ -141,6 +143,7 @@ def default_comm():
 
 # debug hook (tools / bench FRR_BENCH_DEBUG): (label, perf_counter) marks
 TRACE = None
+FALLBACKS = 0  # narrowed selects that fell back to the full data (diagnostics)
 
 
 def _mark(label):
@@ -273,17 +276,65 @@ def select_start(stats, index_base: int, k: int, ops, comm, prefilter: bool = Tr
             comm.all_reduce_(over)
             comm.all_reduce_(tot)
         job = _full_start(c_val, 0, k, ops, comm, idx_map=c_idx)
+        rb = _Readback.of(job, over, tot) if comm.world == 1 else None
 
         def finish():
-            if int(over.item()) == 0 and int(tot.item()) >= k:
-                res = _full_finish(job, comm)
+            if rb is not None:
+                n, bits, ov, tt = rb.values()
+            else:
+                n, bits, ov, tt = None, None, int(over.item()), int(tot.item())
+            if ov == 0 and tt >= k:
+                res = _full_finish(job, comm, n, bits)
                 _mark("narrowed ok")
                 return res
+            global FALLBACKS
+            FALLBACKS += 1
             return _full_finish(_full_start(stats, index_base, k, ops, comm), comm)
 
         return SelectJob(finish)
     job = _full_start(stats, index_base, k, ops, comm)
-    return SelectJob(lambda: _full_finish(job, comm))
+    rb = _Readback.of(job) if comm.world == 1 else None
+    if rb is None:
+        return SelectJob(lambda: _full_finish(job, comm))
+    return SelectJob(lambda: _full_finish(job, comm, *rb.values()[:2]))
+
+
+class _Readback:
+    """The select's result scalars (count, threshold bits, and for the
+    narrowing its overflow flag and total) copied to page-locked host memory
+    in stream order right behind the select's kernels, with an event: a
+    later finish() waits for that event only, not for work enqueued after
+    the select (the bench keeps later passes queued behind it)."""
+
+    SLOTS = 64  # read-backs alive at once (the bench keeps 4 selects in flight)
+    _ring = None
+    _next = 0
+
+    def __init__(self, tensors):
+        torch = N.torch_mod()
+        cls = type(self)
+        if cls._ring is None:
+            # one page-locked block for all slots, allocated once: a fresh
+            # page-locked allocation (cudaHostAlloc) can stall the host for
+            # tens of ms, which must not happen while a pipeline is running
+            cls._ring = torch.empty((cls.SLOTS, 4), dtype=torch.int64, pin_memory=True)
+        self.host = cls._ring[cls._next % cls.SLOTS, : len(tensors)]
+        cls._next += 1
+        for i, t in enumerate(tensors):
+            self.host[i : i + 1].copy_(t.reshape(-1)[:1], non_blocking=True)
+        self.ev = torch.cuda.Event()
+        self.ev.record()
+
+    @classmethod
+    def of(cls, job, *extra):
+        idx, val, n_out, st = job[:4]
+        if not n_out.is_cuda:
+            return None
+        return cls([n_out, st[0:1], *extra])
+
+    def values(self):
+        self.ev.synchronize()
+        return [int(v) for v in self.host.tolist()]
 
 
 def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
@@ -312,20 +363,31 @@ def _full_start(stats, index_base: int, k: int, ops, comm, idx_map=None):
         quota = torch.clamp(ops.k_rem(st) - before, min=0)
         quota = torch.minimum(quota, eq[comm.rank : comm.rank + 1]).contiguous()
     idx, val, n_out = ops.compact(stats, index_base, st, quota, cap=k)
+    if idx_map is not None:
+        # map to global indices now, in stream order (entries past the count
+        # are unwritten: clamped into range, sliced off at the read-back)
+        idx = idx_map[idx.clamp(0, max(0, idx_map.shape[0] - 1))]
+        idx_map = None
     _mark("final launched")
     return idx, val, n_out, st, ops, idx_map
 
 
-def _full_finish(job, comm):
-    """Read back the select enqueued by _full_start: (indices, values, threshold)."""
+def _full_finish(job, comm, n=None, bits=None):
+    """Read back the select enqueued by _full_start: (indices, values,
+    threshold); n and bits: the count and threshold bits when a _Readback
+    already has them (world 1)."""
     torch = N.torch_mod()
     idx, val, n_out, st, ops, idx_map = job
-    thr = ops.threshold(st)
+    if bits is None:
+        thr = ops.threshold(st)
+    else:
+        thr = float(np.array([bits & ((1 << 64) - 1)], dtype=np.uint64).view(np.float64)[0])
     _mark("final read")
-    if idx_map is not None:
-        idx = idx_map[idx[: int(n_out.item())]]
-    if comm.world == 1:
+    if n is None:
         n = int(n_out.item())
+    if idx_map is not None:
+        idx = idx_map[idx[:n]]
+    if comm.world == 1:
         return idx[:n], val[:n], thr
     sizes = torch.stack(comm.all_gather(n_out)).reshape(-1)
     size_list = [int(s) for s in sizes.tolist()]
