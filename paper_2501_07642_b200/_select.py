@@ -276,15 +276,15 @@ def select_start(stats, index_base: int, k: int, ops, comm, prefilter: bool = Tr
             comm.all_reduce_(over)
             comm.all_reduce_(tot)
         job = _full_start(c_val, 0, k, ops, comm, idx_map=c_idx)
-        rb = _Readback.of(job, over, tot) if comm.world == 1 else None
+        rb = _Readback.of(job, over, tot)
 
         def finish():
             if rb is not None:
-                n, bits, ov, tt = rb.values()
+                n, bits, ov, tt, sizes = rb.values()
             else:
-                n, bits, ov, tt = None, None, int(over.item()), int(tot.item())
+                n, bits, ov, tt, sizes = None, None, int(over.item()), int(tot.item()), None
             if ov == 0 and tt >= k:
-                res = _full_finish(job, comm, n, bits)
+                res = _full_finish(job, comm, n, bits, sizes)
                 _mark("narrowed ok")
                 return res
             global FALLBACKS
@@ -293,48 +293,65 @@ def select_start(stats, index_base: int, k: int, ops, comm, prefilter: bool = Tr
 
         return SelectJob(finish)
     job = _full_start(stats, index_base, k, ops, comm)
-    rb = _Readback.of(job) if comm.world == 1 else None
+    rb = _Readback.of(job)
     if rb is None:
         return SelectJob(lambda: _full_finish(job, comm))
-    return SelectJob(lambda: _full_finish(job, comm, *rb.values()[:2]))
+
+    def finish_full():
+        n, bits, sizes = rb.values()
+        return _full_finish(job, comm, n, bits, sizes)
+
+    return SelectJob(finish_full)
 
 
 class _Readback:
-    """The select's result scalars (count, threshold bits, and for the
-    narrowing its overflow flag and total) copied to page-locked host memory
-    in stream order right behind the select's kernels, with an event: a
+    """The select's result scalars -- this rank's count, the threshold bits,
+    for the narrowing its overflow flag and total, and under several ranks
+    every rank's count -- copied to page-locked host memory in stream order
+    right behind the select's kernels and collectives, with an event: a
     later finish() waits for that event only, not for work enqueued after
     the select (the bench keeps later passes queued behind it)."""
 
     SLOTS = 64  # read-backs alive at once (the bench keeps 4 selects in flight)
+    WIDTH = 4 + 256  # scalars + up to 256 ranks' counts
     _ring = None
     _next = 0
 
-    def __init__(self, tensors):
+    def __init__(self, scalars, sizes=None):
         torch = N.torch_mod()
         cls = type(self)
         if cls._ring is None:
             # one page-locked block for all slots, allocated once: a fresh
             # page-locked allocation (cudaHostAlloc) can stall the host for
             # tens of ms, which must not happen while a pipeline is running
-            cls._ring = torch.empty((cls.SLOTS, 4), dtype=torch.int64, pin_memory=True)
-        self.host = cls._ring[cls._next % cls.SLOTS, : len(tensors)]
+            cls._ring = torch.empty((cls.SLOTS, cls.WIDTH), dtype=torch.int64, pin_memory=True)
+        n_sizes = 0 if sizes is None else int(sizes.shape[0])
+        self.n_scalars = len(scalars)
+        self.host = cls._ring[cls._next % cls.SLOTS, : len(scalars) + n_sizes]
         cls._next += 1
-        for i, t in enumerate(tensors):
+        for i, t in enumerate(scalars):
             self.host[i : i + 1].copy_(t.reshape(-1)[:1], non_blocking=True)
+        if n_sizes:
+            self.host[len(scalars):].copy_(sizes.reshape(-1), non_blocking=True)
+        self.has_sizes = sizes is not None
         self.ev = torch.cuda.Event()
         self.ev.record()
 
     @classmethod
     def of(cls, job, *extra):
-        idx, val, n_out, st = job[:4]
+        idx, val, n_out, st, ops, idx_map, gathered = job
         if not n_out.is_cuda:
             return None
-        return cls([n_out, st[0:1], *extra])
+        sizes = gathered[0] if gathered is not None else None
+        if sizes is not None and (not sizes.is_cuda or sizes.shape[0] > cls.WIDTH - 4):
+            return None
+        return cls([n_out, st[0:1], *extra], sizes)
 
     def values(self):
+        """[scalars..., sizes list or None]"""
         self.ev.synchronize()
-        return [int(v) for v in self.host.tolist()]
+        v = [int(x) for x in self.host.tolist()]
+        return v[: self.n_scalars] + [v[self.n_scalars:] if self.has_sizes else None]
 
 
 def _select_full(stats, index_base: int, k: int, ops, comm, idx_map=None):
@@ -368,37 +385,38 @@ def _full_start(stats, index_base: int, k: int, ops, comm, idx_map=None):
         # are unwritten: clamped into range, sliced off at the read-back)
         idx = idx_map[idx.clamp(0, max(0, idx_map.shape[0] - 1))]
         idx_map = None
+    gathered = None
+    if comm.world > 1:
+        # the rank-ordered gather, enqueued now with buffers of the maximum
+        # count k (every rank's count is <= k): the host learns the counts
+        # only at the read-back
+        sizes = torch.cat(comm.all_gather(n_out.reshape(1)))
+        pad_i = torch.zeros(k, dtype=idx.dtype, device=idx.device)
+        pad_v = torch.zeros(k, dtype=val.dtype, device=val.device)
+        pad_i[: idx.shape[0]] = idx[:k]
+        pad_v[: val.shape[0]] = val[:k]
+        gathered = (sizes, comm.all_gather(pad_i), comm.all_gather(pad_v))
     _mark("final launched")
-    return idx, val, n_out, st, ops, idx_map
+    return idx, val, n_out, st, ops, idx_map, gathered
 
 
-def _full_finish(job, comm, n=None, bits=None):
+def _full_finish(job, comm, n=None, bits=None, sizes=None):
     """Read back the select enqueued by _full_start: (indices, values,
-    threshold); n and bits: the count and threshold bits when a _Readback
-    already has them (world 1)."""
+    threshold); n, bits and sizes: this rank's count, the threshold bits and
+    every rank's count when a _Readback already has them."""
     torch = N.torch_mod()
-    idx, val, n_out, st, ops, idx_map = job
+    idx, val, n_out, st, ops, idx_map, gathered = job
     if bits is None:
         thr = ops.threshold(st)
     else:
         thr = float(np.array([bits & ((1 << 64) - 1)], dtype=np.uint64).view(np.float64)[0])
     _mark("final read")
-    if n is None:
-        n = int(n_out.item())
-    if idx_map is not None:
-        idx = idx_map[idx[:n]]
     if comm.world == 1:
+        if n is None:
+            n = int(n_out.item())
         return idx[:n], val[:n], thr
-    sizes = torch.stack(comm.all_gather(n_out)).reshape(-1)
-    size_list = [int(s) for s in sizes.tolist()]
-    mx = max(1, max(size_list))
-    pad_i = torch.zeros(mx, dtype=idx.dtype, device=idx.device)
-    pad_v = torch.zeros(mx, dtype=val.dtype, device=val.device)
-    n_local = size_list[comm.rank]
-    pad_i[:n_local] = idx[:n_local]
-    pad_v[:n_local] = val[:n_local]
-    gi = comm.all_gather(pad_i)
-    gv = comm.all_gather(pad_v)
-    out_i = torch.cat([g[:s] for g, s in zip(gi, size_list)])
-    out_v = torch.cat([g[:s] for g, s in zip(gv, size_list)])
+    size_t, gi, gv = gathered
+    size_list = [int(x) for x in (sizes if sizes is not None else size_t.tolist())]
+    out_i = torch.cat([g[:c] for g, c in zip(gi, size_list)])
+    out_v = torch.cat([g[:c] for g, c in zip(gv, size_list)])
     return out_i, out_v, thr
