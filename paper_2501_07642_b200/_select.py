@@ -204,7 +204,7 @@ def _bound_state(sample, k: int, m_total: int, ops):
     return st, k_s / s
 
 
-def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool = True):
+def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool = True, m_total=None):
     """Global k smallest of the sharded statistics.
 
     Returns (indices, values, threshold) on every rank: indices ascending
@@ -216,7 +216,7 @@ def select_k_smallest(stats, index_base: int, k: int, ops, comm, prefilter: bool
     sample), then runs the radix passes and the final compaction on C: two
     passes over the full statistics instead of ten.  Every statistic <= the
     threshold is in C, so the result is the same as on the full data."""
-    return select_start(stats, index_base, k, ops, comm, prefilter).finish()
+    return select_start(stats, index_base, k, ops, comm, prefilter, m_total).finish()
 
 
 class SelectJob:

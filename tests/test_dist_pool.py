@@ -33,7 +33,7 @@ def _patch_compute(setattr_=setattr):
         bal = O.Balance(kernel._zq, kernel._inv_scale_sq)
         return torch.from_numpy(O.c_exact_stats(bal, design.n_treated, lo, count, threads=1))
 
-    def select(stats, lo, k, comm, keep_device=False, keys_seed=None):
+    def select(stats, lo, k, comm, keep_device=False, keys_seed=None, m_total=None):
         idx, val, thr = select_k_smallest(stats, lo, k, NumpySelectOps(), comm)
         if keys_seed is not None:
             keys = np.column_stack([np.full(idx.shape[0], keys_seed, dtype=np.uint64), idx.numpy().astype(np.uint64)])
