@@ -391,7 +391,9 @@ def run_ours(args):
     e2e_s = _max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
     gc.enable()
     h2d = N_UNITS * D_COV * 8 + 2 * D_COV * 8 + 8 * 16  # Zq, colsum, cc, (seeds/state)
-    d2h = pool.n_accepted * 16 + 8 * 4  # accepted draw indices + stats, threshold/count
+    # accepted draw indices + stats, the (seed, draw) keys built on the device,
+    # and the select's result scalars
+    d2h = pool.n_accepted * 16 + pool.n_accepted * 16 + 8 * 4
     assert pool.n_accepted == k and n_acc == k
 
     peaks, src = _peaks()
